@@ -1,0 +1,132 @@
+"""Pins of oracle/scheduler.py, oracle/queues.py and oracle/drivers.py (CPU only)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import drivers, numerics as nx, scheduler as sch
+from oracle.queues import Box, ConservationError
+import workload as wl
+
+
+# ---------------------------------------------------------------- Algorithm 1 (worked examples)
+
+def test_alg1_hand_executed_examples(golden_dir):
+    ex = json.load(open(os.path.join(golden_dir, "alg1_examples.json")))["examples"]
+    for e in ex:
+        sc = sch.defrag_scores(e["Q"], e["W"], e["delta"])
+        got = {f"{b},{k}": s for b, row in enumerate(sc) for k, s in enumerate(row) if s is not None}
+        assert got.keys() == e["scores"].keys()
+        for key, v in e["scores"].items():
+            assert abs(got[key] - v) < 1e-12, key
+        assert sch.defrag(e["Q"], e["W"], e["delta"]) == tuple(e["pick"])
+        assert sch.mtfs(e["Q"]) == tuple(e["mtfs"])
+
+
+def test_alg1_properties_random_states():
+    g = np.random.default_rng(0)
+    for _ in range(1000):
+        NB, NE, W = g.integers(1, 12), g.integers(1, 9), int(g.integers(0, 6))
+        Q = (g.integers(0, 6, (NB, NE)) * (g.random((NB, NE)) < 0.4)).tolist()
+        nonempty = [(b, e) for b in range(NB) for e in range(NE) if Q[b][e] > 0]
+        pick = sch.defrag(Q, W, 0.5)
+        if not nonempty:
+            assert pick is None and sch.mtfs(Q) is None and sch.flfs(Q) is None
+            continue
+        assert pick in nonempty                             # never an empty queue (L285)
+        assert sch.defrag(Q, 0, 0.5) == sch.mtfs(Q)         # W=0 degenerates to MTFS
+        assert sch.flfs(Q) == min(nonempty)
+        if len(nonempty) == 1:
+            assert pick == nonempty[0]
+
+
+def test_alg1_lookahead_prefers_block_before_dense_wave():
+    """With a dense wave at block b+1, a sparse queue at b outranks a bigger one elsewhere
+    (the defragging intent of PAPER.md L297)."""
+    Q = [[0, 0], [0, 0], [3, 0], [20, 20], [0, 0]]
+    assert sch.mtfs(Q) == (3, 0)
+    assert sch.defrag(Q, W=1, delta=0.9) == (2, 0)
+
+
+# ---------------------------------------------------------------- µ-queues
+
+def test_queue_fifo_and_drain_cap():
+    box = Box(L=1, E=2, K=1, S=0, G=1, T=8)
+    box.enqueue(0, 0, [0, 1, 2, 3], [[1], [1], [0], [1]], [[1.0]] * 4)
+    assert [g.token for g in box.drain(0, 0, 1, cap=2)] == [0, 1]
+    assert [g.token for g in box.drain(0, 0, 1)] == [3]
+    assert [g.token for g in box.drain(0, 0, 0)] == [2]
+    assert box.depths(0) == [[0, 0]]
+
+
+def test_counts_equal_router_histogram_and_placement():
+    T, E, K, G = 64, 8, 2, 4
+    z = wl.router_logits(1, 1, G * T, E)[0]
+    idx, w = nx.route_topk(z, K)
+    box = Box(L=1, E=E, K=K, S=0, G=G, T=T)
+    box.enqueue(0, 0, range(G * T), idx, w)
+    hist = np.bincount(idx.ravel(), minlength=E)
+    for e in range(E):
+        q = box.queues[(e % G, 0, e)]
+        assert len(q) == hist[e]
+        assert all(g.home == g.token // T for g in q.q)
+    assert sum(len(q) for q in box.queues.values()) == G * T * K
+
+
+def test_pool_merges_exactly_k_legs():
+    box = Box(L=1, E=2, K=2, S=0, G=1, T=4)
+    assert box.pool.put(3, 0, 1.0) is False
+    assert box.pool.put(3, 1, 2.0) is True
+    assert sorted(box.pool.pop(3)) == [0, 1]
+    with pytest.raises(ConservationError):
+        box.pool.put(1, 0, 0.0); box.pool.put(1, 0, 0.0)
+
+
+# ---------------------------------------------------------------- async == sync
+
+def _tiny_problem(seed, L=2, E=4, K=2, S=0, d=16, ff=32, N=8, dtype="bf16"):
+    h0 = wl.hidden0(seed, N, d, dtype)
+    h0 = wl.f32_from_bf16_bits(h0) if dtype == "bf16" else h0
+    tables = {}
+
+    def logits(p, l):
+        if (p, l) not in tables:
+            tables[(p, l)] = wl.router_logits(seed, L, N, E, pass_idx=p, layers=[l])[0]
+        return tables[(p, l)]
+
+    conv = wl.f32_from_bf16_bits if dtype == "bf16" else (lambda a: a)
+    W = [[tuple(conv(a) for a in wl.expert_weights(seed, l, e, d, ff, dtype)) for e in range(E)]
+         for l in range(L)]
+    SH = [[tuple(conv(a) for a in wl.expert_weights(seed, l, E + j, d, ff, dtype)) for j in range(S)]
+          for l in range(L)] if S else None
+    return h0, logits, W, SH
+
+
+@pytest.mark.parametrize("G,policy,cap,S,dtype", [
+    (1, "defrag", 0, 0, "bf16"), (1, "mtfs", 3, 0, "bf16"), (2, "flfs", 0, 1, "bf16"),
+    (2, "random", 2, 0, "bf16"), (4, "defrag", 5, 0, "bf16"), (4, "random", 0, 1, "fp32"),
+])
+def test_async_equals_sync_bitwise(G, policy, cap, S, dtype):
+    T = 4
+    h0, logits, W, SH = _tiny_problem(G * 10 + cap, S=S, N=G * T, dtype=dtype)
+    ref, _ = drivers.sync_run(h0, logits, W, K=2, n_passes=2, shared=SH, dtype=dtype)
+    for seed in range(3):
+        got, box, n = drivers.async_run(h0, logits, W, K=2, G=G, T=T, n_passes=2, shared=SH,
+                                        dtype=dtype, policy=policy, max_cap=cap, seed=seed)
+        assert n == G * T * 2 * 2
+        assert np.array_equal(got, ref)
+
+
+def test_async_fault_injection_names_the_token():
+    h0, logits, W, _ = _tiny_problem(3, N=8)
+    with pytest.raises(ConservationError, match="token 5"):
+        drivers.async_run(h0, logits, W, K=2, G=2, T=4, n_passes=1, seed=1,
+                          fault_drop=(5, 1, 0, 1))
+
+
+def test_async_every_leg_drained_once():
+    h0, logits, W, _ = _tiny_problem(4, N=8, L=3)
+    _, box, _ = drivers.async_run(h0, logits, W, K=2, G=2, T=4, n_passes=2, seed=2, max_cap=2)
+    drained = [(g.token, g.layer, g.pass_idx, g.k) for (_, _, _, legs) in box.trace_drain for g in legs]
+    assert len(drained) == len(set(drained)) == 8 * 3 * 2 * 2

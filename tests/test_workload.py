@@ -1,0 +1,31 @@
+"""The seeded input generator: determinism, rank slicing, distributions (CPU only)."""
+import numpy as np
+
+import workload as wl
+
+
+def test_generator_is_deterministic_and_slices_by_rank():
+    a = wl.router_logits(3, L=2, T=64, E=8)
+    b = wl.router_logits(3, L=2, T=64, E=8)
+    assert a.tobytes() == b.tobytes()
+    s = wl.router_logits(3, L=2, T=32, E=8, token_offset=32)
+    assert np.array_equal(s, a[:, 32:])
+    assert np.array_equal(wl.hidden0(1, 10, 16, token_offset=6), wl.hidden0(1, 16, 16)[6:])
+    w1, w3, w2 = wl.expert_weights(0, 1, 2, 32, 48)
+    assert w1.shape == (48, 32) and w3.shape == (48, 32) and w2.shape == (32, 48)
+    assert w1.dtype == np.uint16 and not np.array_equal(w1, w3)
+
+
+def test_zipf_probs_and_skew_epochs():
+    p = wl.zipf_probs(8, 1.2)
+    assert abs(p.sum() - 1) < 1e-15 and np.all(np.diff(p) < 0)
+    assert abs(p[0] / p[1] - 2 ** 1.2) < 1e-12
+    assert wl.skew_epoch(0, 31, 32, 1000) == 0 and wl.skew_epoch(31, 8, 32, 1000) == 1
+    assert not np.array_equal(wl.layer_perm(0, 0, 0, 64), wl.layer_perm(0, 0, 1, 64))
+    assert np.array_equal(np.sort(wl.layer_perm(0, 5, 2, 64)), np.arange(64))
+
+
+def test_weight_scales():
+    w1, _, w2 = wl.expert_weights(0, 0, 0, 512, 1024, dtype="fp32")
+    assert abs(w1.std() - 512 ** -0.5) < 0.01 * 512 ** -0.5 * 10
+    assert abs(w2.std() - 1024 ** -0.5) < 0.01 * 1024 ** -0.5 * 10
