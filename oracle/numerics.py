@@ -94,12 +94,17 @@ def expert_ffn(x: np.ndarray, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray,
     Each output row depends only on its own input row (no cross-row arithmetic), which is what
     makes asynchronous re-batching return the synchronous result.
     """
+    A = swiglu_act(x, w1, w3, dtype)
+    O = (A.astype(np.float64) @ np.asarray(w2, np.float64).T).astype(np.float32)
+    return to_storage(O, dtype)
+
+
+def swiglu_act(x: np.ndarray, w1: np.ndarray, w3: np.ndarray, dtype: str = "bf16") -> np.ndarray:
+    """The expert's hidden activation A = store(silu(fp32(W1·x)) ⊙ fp32(W3·x)), [n, ff]."""
     x64 = np.asarray(x, dtype=np.float64)
     G = (x64 @ np.asarray(w1, np.float64).T).astype(np.float32)
     U = (x64 @ np.asarray(w3, np.float64).T).astype(np.float32)
-    A = to_storage(silu(G) * U.astype(np.float64), dtype)
-    O = (A.astype(np.float64) @ np.asarray(w2, np.float64).T).astype(np.float32)
-    return to_storage(O, dtype)
+    return to_storage(silu(G) * U.astype(np.float64), dtype)
 
 
 # ----------------------------------------------------------------------------- a8: combine

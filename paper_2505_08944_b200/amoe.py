@@ -1,0 +1,355 @@
+"""Thin Python binding of libamoe (include/amoe.h): argument marshalling only.
+
+Every step of the hot path runs in libamoe's CUDA kernels. PyTorch provides device memory,
+streams and (multi-GPU) process groups / symmetric memory. If the shared library is missing
+this module raises at import-time use — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+MAX_G, MAX_E, MAX_GROUP = 8, 256, 128
+BF16, FP32 = 0, 1
+DEFRAG, MTFS, FLFS = 0, 1, 2
+POLICIES = {"defrag": DEFRAG, "mtfs": MTFS, "flfs": FLFS}
+BUF = dict(h=0, x=1, pool=2, tok_w=3, tok_idx=4, tok_layer=5, tok_pass=6, rings=7, qctr=8, stats=9, scratch=10)
+STATUS = {0: "OK", 1: "IDLE", 2: "EINVAL", 3: "ENOTHOSTED", 4: "ECUDA", 5: "EDEVICE", 6: "EPEER", 7: "ENOMEM"}
+FAULTS = {1: "ring overflow", 2: "leg count > K+S", 3: "expert index out of range", 4: "not hosted",
+          5: "combine ring overflow", 6: "token slot out of range", 7: "stale/unpublished ring entry",
+          8: "no router table"}
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libamoe.so")
+
+
+class Config(C.Structure):
+    _fields_ = [("L", C.c_int32), ("E", C.c_int32), ("K", C.c_int32), ("S", C.c_int32), ("d", C.c_int32),
+                ("ff", C.c_int32), ("G", C.c_int32), ("rank", C.c_int32), ("T_slots", C.c_int32),
+                ("dtype", C.c_int32), ("max_batch", C.c_int32), ("rows_cap", C.c_int32),
+                ("rms_eps", C.c_float), ("owner", C.c_int32 * MAX_E)]
+
+
+class Leg(C.Structure):
+    _fields_ = [("token_slot", C.c_int32), ("k", C.c_int16), ("home", C.c_int16), ("w", C.c_float),
+                ("seq", C.c_uint32)]
+
+
+class Group(C.Structure):
+    _fields_ = [("nq", C.c_int32), ("layer", C.c_int32 * MAX_GROUP), ("expert", C.c_int32 * MAX_GROUP),
+                ("rows_cap", C.c_int32), ("tile", C.c_void_p), ("meta", C.c_void_p), ("qinfo", C.c_void_p),
+                ("act", C.c_void_p), ("out", C.c_void_p)]
+
+
+class RunParams(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("W", C.c_int32), ("delta", C.c_float), ("grouped", C.c_int32),
+                ("max_picks", C.c_int32)]
+
+
+class RunStats(C.Structure):
+    _fields_ = [("picks", C.c_int64), ("queues_run", C.c_int64), ("legs", C.c_int64),
+                ("token_layers", C.c_int64), ("kernel_launches", C.c_int64), ("idle_polls", C.c_int64)]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+EXPORTS = {
+    "amoe_workspace_bytes": (C.c_size_t, [C.POINTER(Config)]),
+    "amoe_create": (C.c_int, [C.POINTER(Config), C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "amoe_import_peers": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
+    "amoe_set_expert": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "amoe_set_router": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "amoe_token_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
+    "amoe_enqueue": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p]),
+    "amoe_queue_depths": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p]),
+    "amoe_pick": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_float,
+                            C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "amoe_schedule": (C.c_int, [C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
+                                C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "amoe_rebatch": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_int, C.c_void_p]),
+    "amoe_expert_ffn": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
+    "amoe_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
+    "amoe_combine": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "amoe_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, C.POINTER(RunStats), C.c_void_p]),
+    "amoe_pass_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(RunParams),
+                                 C.POINTER(RunStats), C.c_void_p]),
+    "amoe_get_buffer": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "amoe_hosted": (C.c_int, [C.c_void_p]),
+    "amoe_ring_cap": (C.c_int, [C.c_void_p]),
+    "amoe_local_queue": (C.c_int, [C.c_void_p, C.c_int]),
+    "amoe_scratch_group": (C.c_int, [C.c_void_p, C.POINTER(Group)]),
+    "amoe_launch_count": (C.c_int64, [C.c_void_p]),
+    "amoe_check": (C.c_int, [C.c_void_p]),
+    "amoe_error_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
+    "amoe_clear_error": (C.c_int, [C.c_void_p]),
+    "amoe_status_string": (C.c_char_p, [C.c_int]),
+    "amoe_destroy": (C.c_int, [C.c_void_p]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libamoe.so (build it with `python -m paper_2505_08944_b200.build`). Raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"libamoe.so not found at {path}: run `python -m paper_2505_08944_b200.build` "
+                               "(there is no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(lib, name)
+            f.restype, f.argtypes = res, args
+        _lib = lib
+    return _lib
+
+
+class AmoeError(RuntimeError):
+    def __init__(self, status, what, info=None):
+        msg = f"{what}: {STATUS.get(status, status)}"
+        if info is not None and info[0]:
+            msg += f" (device fault {info[0]} '{FAULTS.get(info[0], '?')}' args {list(info[1:])})"
+        super().__init__(msg)
+        self.status = status
+        self.info = info
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def make_config(L, E, K, S, d, ff, T_slots, G=1, rank=0, dtype="bf16", max_batch=0, rows_cap=0, owner=None,
+                rms_eps=1e-6) -> Config:
+    cfg = Config()
+    cfg.L, cfg.E, cfg.K, cfg.S, cfg.d, cfg.ff = L, E, K, S, d, ff
+    cfg.G, cfg.rank, cfg.T_slots = G, rank, T_slots
+    cfg.dtype = BF16 if dtype == "bf16" else FP32
+    cfg.max_batch, cfg.rows_cap, cfg.rms_eps = max_batch, rows_cap, rms_eps
+    own = [e % G for e in range(E)] if owner is None else list(owner)
+    for e in range(E):
+        cfg.owner[e] = own[e]
+    return cfg
+
+
+def workspace_bytes(cfg: Config) -> int:
+    return int(load().amoe_workspace_bytes(C.byref(cfg)))
+
+
+def schedule(Q, n_experts, policy="defrag", W=4, delta=0.5):
+    """Host scheduler (Algorithm 1 / MTFS / FLFS) on a [blocks, queues] depth array; None = idle."""
+    import numpy as np
+    q = np.ascontiguousarray(Q, dtype=np.uint32)
+    b, e = C.c_int(), C.c_int()
+    st = load().amoe_schedule(q.ctypes.data_as(C.POINTER(C.c_uint32)), q.shape[0], q.shape[1], n_experts,
+                              POLICIES[policy], W, delta, C.byref(b), C.byref(e))
+    if st not in (0, 1):
+        raise AmoeError(st, "amoe_schedule")
+    return None if st == 1 else (b.value, e.value)
+
+
+class GroupBuffers:
+    """Caller-owned device buffers of one grouped execution (amoe_group)."""
+
+    def __init__(self, ctx: "Context", rows_cap: int):
+        dev, tdt = ctx.device, ctx.torch_dtype
+        self.rows_cap = rows_cap
+        self.tile = torch.zeros(rows_cap, ctx.d, dtype=tdt, device=dev)
+        self.meta = torch.zeros(rows_cap, 4, dtype=torch.int32, device=dev)
+        self.qinfo = torch.zeros(3 * MAX_GROUP, dtype=torch.int32, device=dev)
+        self.act = torch.zeros(rows_cap, ctx.ff, dtype=tdt, device=dev)
+        self.out = torch.zeros(rows_cap, ctx.d, dtype=tdt, device=dev)
+        self.g = Group()
+        self.g.rows_cap = rows_cap
+        self.g.tile, self.g.meta, self.g.qinfo = self.tile.data_ptr(), self.meta.data_ptr(), self.qinfo.data_ptr()
+        self.g.act, self.g.out = self.act.data_ptr(), self.out.data_ptr()
+
+    def set_queues(self, pairs):
+        self.g.nq = len(pairs)
+        for i, (l, e) in enumerate(pairs):
+            self.g.layer[i], self.g.expert[i] = l, e
+        return self
+
+    def info(self):
+        """(n, row_off, start) per queue, on the host."""
+        q = self.qinfo.cpu().numpy()
+        nq = self.g.nq
+        return q[:nq], q[MAX_GROUP:MAX_GROUP + nq], q[2 * MAX_GROUP:2 * MAX_GROUP + nq]
+
+
+class Context:
+    """One libamoe context (one rank). The workspace is a caller-owned torch uint8 tensor."""
+
+    def __init__(self, cfg: Config, workspace: torch.Tensor | None = None, device=None):
+        self.lib = load()
+        self.cfg = cfg
+        self.device = torch.device(device or "cuda")
+        nbytes = workspace_bytes(cfg)
+        if nbytes == 0:
+            raise AmoeError(2, "amoe_workspace_bytes (invalid config)")
+        if workspace is None:
+            workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = workspace.data_ptr()
+        pad = (-base) % 256
+        self.ws_tensor = workspace
+        self.ws = workspace[pad:pad + nbytes]
+        self.ws_bytes = nbytes
+        h = C.c_void_p()
+        self._chk(self.lib.amoe_create(C.byref(cfg), C.c_void_p(self.ws.data_ptr()), nbytes, C.byref(h)), "amoe_create")
+        self.h = h
+        self.L, self.E, self.K, self.S, self.d, self.ff = cfg.L, cfg.E, cfg.K, cfg.S, cfg.d, cfg.ff
+        self.T, self.G, self.rank = cfg.T_slots, cfg.G, cfg.rank
+        self.dtype = "bf16" if cfg.dtype == BF16 else "fp32"
+        self.torch_dtype = torch.bfloat16 if cfg.dtype == BF16 else torch.float32
+        self.H = self.lib.amoe_hosted(h)
+        self._keep = []
+        if cfg.G == 1:
+            self.import_peers([self.ws.data_ptr()])
+
+    # -- errors
+    def _chk(self, st, what, ok=(0,)):
+        if st not in ok:
+            info = None
+            if st == 5 and getattr(self, "h", None) is not None:
+                info = self.error_info()
+            raise AmoeError(st, what, info)
+        return st
+
+    def error_info(self):
+        arr = (C.c_uint32 * 4)()
+        self.lib.amoe_error_info(self.h, arr)
+        return list(arr)
+
+    def check(self):
+        return self._chk(self.lib.amoe_check(self.h), "amoe_check")
+
+    def clear_error(self):
+        self.lib.amoe_clear_error(self.h)
+
+    # -- setup
+    def import_peers(self, ptrs):
+        arr = (C.c_uint64 * len(ptrs))(*ptrs)
+        self._chk(self.lib.amoe_import_peers(self.h, arr, len(ptrs)), "amoe_import_peers")
+
+    def set_expert(self, layer, expert, w1, w3, w2):
+        self._keep.append((w1, w3, w2))
+        return self._chk(self.lib.amoe_set_expert(self.h, layer, expert, _p(w1), _p(w3), _p(w2)), "amoe_set_expert")
+
+    def set_router(self, table: torch.Tensor):
+        assert table.dtype == torch.float32 and table.is_contiguous()
+        self._router = table
+        n_tab = table.numel() // (self.L * self.T * self.E)
+        self._chk(self.lib.amoe_set_router(self.h, _p(table), n_tab), "amoe_set_router")
+
+    def local_queue(self, expert):
+        return self.lib.amoe_local_queue(self.h, expert)
+
+    def ring_cap(self):
+        return self.lib.amoe_ring_cap(self.h)
+
+    def launch_count(self):
+        return int(self.lib.amoe_launch_count(self.h))
+
+    # -- hot path calls
+    def token_init(self, slots, h0, pass_idx=0, stream=None):
+        self._chk(self.lib.amoe_token_init(self.h, _p(slots), slots.numel(), _p(h0), pass_idx, _stream(stream)),
+                  "amoe_token_init")
+
+    def enqueue(self, layer, slots, logits=None, topk_idx=None, topk_w=None, stream=None):
+        self._chk(self.lib.amoe_enqueue(self.h, layer, _p(slots), slots.numel(), _p(logits), _p(topk_idx),
+                                        _p(topk_w), _stream(stream)), "amoe_enqueue")
+
+    def queue_depths(self, stream=None):
+        import numpy as np
+        out = (C.c_uint32 * (self.L * self.H))()
+        self._chk(self.lib.amoe_queue_depths(self.h, out, _stream(stream)), "amoe_queue_depths")
+        return np.array(out, dtype=np.uint32).reshape(self.L, self.H)
+
+    def pick(self, Q, policy="defrag", W=4, delta=0.5):
+        import numpy as np
+        q = np.ascontiguousarray(Q, dtype=np.uint32)
+        arr = q.ctypes.data_as(C.POINTER(C.c_uint32))
+        b, e = C.c_int(), C.c_int()
+        st = self._chk(self.lib.amoe_pick(self.h, arr, POLICIES[policy], W, delta, C.byref(b), C.byref(e)),
+                       "amoe_pick", ok=(0, 1))
+        return None if st == 1 else (b.value, e.value)
+
+    def rebatch(self, gb: GroupBuffers, max_tokens=0, stream=None):
+        self._chk(self.lib.amoe_rebatch(self.h, C.byref(gb.g), max_tokens, _stream(stream)), "amoe_rebatch")
+
+    def expert_ffn(self, gb: GroupBuffers, stream=None):
+        self._chk(self.lib.amoe_expert_ffn(self.h, C.byref(gb.g), _stream(stream)), "amoe_expert_ffn")
+
+    def forward(self, gb: GroupBuffers, stream=None):
+        self._chk(self.lib.amoe_forward(self.h, C.byref(gb.g), _stream(stream)), "amoe_forward")
+
+    def combine(self, retire_pass, stream=None):
+        self._chk(self.lib.amoe_combine(self.h, retire_pass, _stream(stream)), "amoe_combine")
+
+    def run(self, retire_pass, policy="defrag", W=4, delta=0.5, grouped=True, max_picks=0, stream=None):
+        p = RunParams(POLICIES[policy], W, delta, 1 if grouped else 0, max_picks)
+        st = RunStats()
+        self._chk(self.lib.amoe_run(self.h, C.byref(p), retire_pass, C.byref(st), _stream(stream)), "amoe_run")
+        return st.as_dict()
+
+    def pass_host(self, h0_host: torch.Tensor, h_out_host: torch.Tensor, pass_idx=0, policy="defrag", W=4,
+                  delta=0.5, grouped=True, stream=None):
+        p = RunParams(POLICIES[policy], W, delta, 1 if grouped else 0, 0)
+        st = RunStats()
+        self._chk(self.lib.amoe_pass_host(self.h, _p(h0_host), _p(h_out_host), pass_idx, C.byref(p), C.byref(st),
+                                          _stream(stream)), "amoe_pass_host")
+        return st.as_dict()
+
+    # -- introspection
+    def buffer(self, name, dtype=None, shape=None):
+        ptr, nbytes = C.c_void_p(), C.c_size_t()
+        self._chk(self.lib.amoe_get_buffer(self.h, BUF[name], C.byref(ptr), C.byref(nbytes)), "amoe_get_buffer")
+        off = ptr.value - self.ws.data_ptr()
+        t = self.ws[off:off + nbytes.value]
+        if dtype is not None:
+            t = t.view(dtype)
+        if shape is not None:
+            t = t.view(*shape)
+        return t
+
+    def state(self):
+        """Named views of the token state (home rank)."""
+        td = self.torch_dtype
+        return dict(
+            h=self.buffer("h", td, (self.T, self.d)), x=self.buffer("x", td, (self.T, self.d)),
+            pool=self.buffer("pool", td, (self.T, self.K + self.S, self.d)),
+            tok_w=self.buffer("tok_w", torch.float32, (self.T, self.K)),
+            tok_idx=self.buffer("tok_idx", torch.int32, (self.T, self.K)),
+            tok_layer=self.buffer("tok_layer", torch.int32, (self.T,)),
+            tok_pass=self.buffer("tok_pass", torch.int32, (self.T,)),
+            qctr=self.buffer("qctr", torch.int32, (self.L, self.H, 4)),
+            stats=self.buffer("stats", torch.int64, (8,)),
+        )
+
+    def ring(self, layer, local_q):
+        cap = self.ring_cap()
+        r = self.buffer("rings", torch.int32, (self.L * self.H, cap, 4))
+        return r[layer * self.H + local_q]
+
+    def scratch_group(self):
+        g = Group()
+        self._chk(self.lib.amoe_scratch_group(self.h, C.byref(g)), "amoe_scratch_group")
+        return g
+
+    def close(self):
+        if getattr(self, "h", None) is not None:
+            self.lib.amoe_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,218 @@
+// amoe_internal.cuh — workspace layout, device context and memory-ordering helpers shared by
+// the libamoe kernels (sm_100a). Not part of the C ABI (see include/amoe.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "amoe.h"
+
+namespace amoe {
+
+constexpr int kWarp = 32;
+constexpr int kMaxKS = 12;          // K + S legs per token
+constexpr int kRowAlign = 128;      // group rows are allocated per queue in multiples of this
+
+// Device fault codes latched into the error word.
+enum Fault : uint32_t {
+  F_NONE = 0,
+  F_RING_OVERFLOW = 1,    // args: queue, reserve, head
+  F_LEG_OVERCOUNT = 2,    // args: home slot, count, k
+  F_EXPERT_RANGE = 3,     // args: slot, expert, layer
+  F_NOT_HOSTED = 4,       // args: layer, expert, rank
+  F_CRING_OVERFLOW = 5,   // args: reserve, head
+  F_SLOT_RANGE = 6,       // args: slot, T
+  F_STALE_ENTRY = 7,      // args: queue, position, seq
+  F_NO_ROUTER = 8,        // args: slot, layer, pass (combine needs amoe_set_router)
+};
+
+// Byte offsets of every object inside a rank's workspace. Identical on every rank (the
+// layout depends only on the config), so a peer object's address is peer_base + offset.
+struct Layout {
+  uint64_t err;        // u32[8]: code, a0, a1, a2
+  uint64_t stats;      // u64[8]: 0 merges, 1 retired, 2 legs executed, 3 legs sent remote
+  uint64_t done;       // u32[AMOE_MAX_G]: done epoch per rank (written by that rank)
+  uint64_t qctr;       // u32[L*H][4]: reserve, commit, head, pad
+  uint64_t rings;      // amoe_leg[L*H][ring_cap]
+  uint64_t cctr;       // u32[4]: combine ring reserve, commit, head, pad
+  uint64_t cring;      // amoe_leg[cring_cap]
+  uint64_t cinfo;      // i32[4]: combine drain n, start
+  uint64_t h, x;       // [T][d]
+  uint64_t pool;       // [T][K+S][d]
+  uint64_t legs_done;  // u32[T]
+  uint64_t tok_layer;  // i32[T]
+  uint64_t tok_pass;   // i32[T]
+  uint64_t tok_w;      // f32[T][K]
+  uint64_t tok_idx;    // i32[T][K]
+  uint64_t wmaps;      // CUtensorMap[L*H][3]
+  uint64_t wptrs;      // u64[L*H][3]
+  uint64_t s_tile, s_meta, s_qinfo, s_act, s_out;   // amoe_run's group scratch
+  uint64_t total;
+  int32_t rows_cap;
+  int32_t pad_;
+};
+
+// Everything a kernel needs to address local and peer objects. Passed by value (param space).
+struct DevCtx {
+  int32_t L, E, K, S, d, ff, G, rank, T, dtype, H, Hr, KS, esize;
+  uint32_t ring_cap, ring_mask, cring_cap, cring_mask;
+  float eps;
+  int32_t n_tab;
+  const float* router;               // local [n_tab][L][T][E] or null
+  Layout lay;
+  uint64_t peer[AMOE_MAX_G];         // workspace base per rank; peer[rank] = local
+  int16_t lq[AMOE_MAX_E];            // local queue index of routed expert e on its owner
+  uint8_t owner[AMOE_MAX_E];
+};
+
+// One grouped execution as the queue kernels see it.
+struct GroupDev {
+  int32_t nq;
+  int32_t rows_cap;
+  int32_t max_tokens;
+  int32_t* qinfo;          // [3*AMOE_MAX_GROUP]: n, row_off, start
+  amoe_leg* meta;
+  void* tile;
+  void* out;
+  int32_t qid[AMOE_MAX_GROUP];   // local queue index l*H + lq
+};
+
+// Grouped FFN launch description (tensor-core path).
+struct FfnLaunch {
+  int nq;
+  const int32_t* qinfo;
+  const CUtensorMap* wmaps;      // device [L*H][3]
+  int wslot[AMOE_MAX_GROUP];     // (l*H + lq) * 3
+};
+
+template <typename T>
+__device__ __forceinline__ T* wsp(const DevCtx& c, int r, uint64_t off) {
+  return reinterpret_cast<T*>(c.peer[r] + off);
+}
+
+// ------------------------------------------------------------------ memory-ordering helpers
+// Local objects use .gpu scope; objects on (or shared with) a peer GPU use .sys scope so the
+// NVLink peer observes the ordering (PTX memory model, scopes).
+
+__device__ __forceinline__ uint32_t atom_add_relaxed(uint32_t* p, uint32_t v, bool sys) {
+  uint32_t old;
+  if (sys) asm volatile("atom.relaxed.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  else     asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t* p, uint32_t v, bool sys) {
+  uint32_t old;
+  if (sys) asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  else     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v, bool sys) {
+  if (sys) asm volatile("red.release.sys.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+  else     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v, bool sys) {
+  if (sys) asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+  else     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_sc(bool sys) {
+  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else     asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Latch the first device fault (later faults keep the first one's arguments).
+__device__ __forceinline__ void raise_fault(const DevCtx& c, uint32_t code, uint32_t a0, uint32_t a1,
+                                            uint32_t a2) {
+  uint32_t* e = wsp<uint32_t>(c, c.rank, c.lay.err);
+  if (atomicCAS(e, 0u, code) == 0u) {
+    e[1] = a0; e[2] = a1; e[3] = a2;
+    __threadfence();
+  }
+}
+
+// ------------------------------------------------------------------ µ-queue rings
+
+__device__ __forceinline__ uint32_t* qctr_ptr(const DevCtx& c, int r, int q) {
+  return wsp<uint32_t>(c, r, c.lay.qctr) + 4 * q;
+}
+__device__ __forceinline__ amoe_leg* ring_ptr(const DevCtx& c, int r, int q) {
+  return wsp<amoe_leg>(c, r, c.lay.rings) + (uint64_t)q * c.ring_cap;
+}
+
+// Write one leg into slot `pos` of a ring (the seq field is the publication flag, last).
+__device__ __forceinline__ void write_leg(amoe_leg* ring, uint32_t mask, uint32_t pos,
+                                          const amoe_leg& g, bool sys) {
+  amoe_leg* e = ring + (pos & mask);
+  int2 a;
+  a.x = g.token_slot;
+  a.y = (int)((uint32_t)(uint16_t)g.k | ((uint32_t)(uint16_t)g.home << 16));
+  *reinterpret_cast<int2*>(e) = a;
+  e->w = g.w;
+  st_release(&e->seq, pos + 1u, sys);
+}
+
+// ------------------------------------------------------------------ storage-type vectors
+// 16-byte vectors: 8 bf16 or 4 fp32 values.
+
+template <typename T> struct Vec;
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void load(const __nv_bfloat16* p, float* f) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { float2 t = __bfloat1622float2(b[i]); f[2 * i] = t.x; f[2 * i + 1] = t.y; }
+  }
+  __device__ __forceinline__ static void store(__nv_bfloat16* p, const float* f) {
+    uint4 u;
+    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+  // value as stored (rounded), for sums over stored values
+  __device__ __forceinline__ static float round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+};
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void load(const float* p, float* f) {
+    float4 u = *reinterpret_cast<const float4*>(p);
+    f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w;
+  }
+  __device__ __forceinline__ static void store(float* p, const float* f) {
+    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+  }
+  __device__ __forceinline__ static float round(float v) { return v; }
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Copy `bytes` (multiple of 16) with a warp, 16 B per lane, 4 loads in flight per lane.
+__device__ __forceinline__ void warp_copy(void* dst, const void* src, int bytes, int lane) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const int n = bytes >> 4;
+  int i = lane;
+  for (; i + 96 < n; i += 128) {
+    uint4 a = s[i], b = s[i + 32], c2 = s[i + 64], e = s[i + 96];
+    d[i] = a; d[i + 32] = b; d[i + 64] = c2; d[i + 96] = e;
+  }
+  for (; i < n; i += 32) d[i] = s[i];
+}
+
+}  // namespace amoe

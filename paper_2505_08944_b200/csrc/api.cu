@@ -1,0 +1,657 @@
+// api.cu — host side of libamoe: the C ABI of include/amoe.h, the workspace layout, TMA
+// descriptor encoding, and the asynchronous scheduler loop (amoe_run).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <thread>
+#include <vector>
+
+#include "amoe_internal.cuh"
+
+namespace amoe {
+// kernels (k_*.cu)
+int launch_token_init(const DevCtx&, const int32_t*, int, const void*, int, cudaStream_t);
+int launch_enqueue(const DevCtx&, int, const int32_t*, int, const float*, const int32_t*, const float*, cudaStream_t);
+int launch_combine(const DevCtx&, int, cudaStream_t);
+int launch_announce(const DevCtx&, uint32_t, cudaStream_t);
+int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
+int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
+int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
+int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, int, cudaStream_t);
+int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
+int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
+}  // namespace amoe
+
+using namespace amoe;
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct MapCacheEntry {
+  const void* ptr;
+  int rows, cols, box_rows;
+  CUtensorMap map;
+};
+
+struct amoe_ctx {
+  amoe_config cfg;
+  DevCtx dc;
+  Layout lay;
+  char* ws;
+  size_t ws_bytes;
+  int num_sms;
+  int Hr, H;
+  std::vector<int> hosted_flags;      // [L*H] weights registered
+  std::vector<uint64_t> wptrs;        // [L*H*3]
+  uint32_t* pinned;                   // snapshot buffer (header + qctr)
+  size_t snap_bytes;
+  int64_t launches;
+  int64_t admitted;
+  uint64_t retired_base;
+  uint32_t epoch;
+  cudaStream_t last_stream;
+  std::vector<MapCacheEntry> map_cache;
+  int32_t* scratch_qinfo;
+};
+
+static PFN_encodeTiled get_encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2D bf16 row-major matrix [rows, cols] -> TMA map with a {64, box_rows} box, 128-B swizzle.
+static bool encode_bf16_2d(CUtensorMap* m, const void* ptr, int rows, int cols, int box_rows) {
+  PFN_encodeTiled enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static const CUtensorMap* cached_map(amoe_ctx* c, const void* ptr, int rows, int cols, int box_rows) {
+  for (auto& e : c->map_cache)
+    if (e.ptr == ptr && e.rows == rows && e.cols == cols && e.box_rows == box_rows) return &e.map;
+  MapCacheEntry e{ptr, rows, cols, box_rows, {}};
+  if (!encode_bf16_2d(&e.map, ptr, rows, cols, box_rows)) return nullptr;
+  if (c->map_cache.size() > 64) c->map_cache.erase(c->map_cache.begin());
+  c->map_cache.push_back(e);
+  return &c->map_cache.back().map;
+}
+
+static uint32_t next_pow2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return (uint32_t)p;
+}
+
+static inline uint64_t al(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+static bool valid_cfg(const amoe_config* c) {
+  if (!c) return false;
+  if (c->L < 1 || c->E < 1 || c->E > AMOE_MAX_E || c->K < 1 || c->K > 8 || c->K > c->E) return false;
+  if (c->S < 0 || c->S > 4 || c->K + c->S > kMaxKS) return false;
+  if (c->d < 64 || c->d % 64 || c->ff < 128 || c->ff % 128) return false;
+  if (c->G < 1 || c->G > AMOE_MAX_G || c->rank < 0 || c->rank >= c->G) return false;
+  if (c->T_slots < 1 || c->dtype < 0 || c->dtype > 1 || c->max_batch < 0 || c->rows_cap < 0) return false;
+  for (int e = 0; e < c->E; ++e)
+    if (c->owner[e] < 0 || c->owner[e] >= c->G) return false;
+  return true;
+}
+
+// owner table: all-zero with G > 1 means the default e mod G
+static void resolve_owner(const amoe_config* c, int* owner) {
+  bool allzero = true;
+  for (int e = 0; e < c->E; ++e) allzero &= c->owner[e] == 0;
+  for (int e = 0; e < c->E; ++e) owner[e] = (allzero && c->G > 1) ? e % c->G : c->owner[e];
+}
+
+static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_t* ring_cap, uint32_t* cring_cap) {
+  int owner[AMOE_MAX_E];
+  resolve_owner(c, owner);
+  int cnt[AMOE_MAX_G] = {0};
+  for (int e = 0; e < c->E; ++e) cnt[owner[e]]++;
+  int Hr = 0;
+  for (int r = 0; r < c->G; ++r) Hr = std::max(Hr, cnt[r]);
+  const int H = Hr + c->S;
+  const uint64_t es = c->dtype == AMOE_BF16 ? 2 : 4;
+  const uint64_t T = c->T_slots, d = c->d, ff = c->ff, KS = c->K + c->S;
+  const uint32_t rc = next_pow2(std::max<uint64_t>((uint64_t)c->G * T, 2));
+  const uint32_t crc = next_pow2(std::max<uint64_t>(T, 2));
+  int rows = c->rows_cap;
+  if (rows == 0) {
+    const uint64_t legs = (uint64_t)c->G * T * (uint64_t)std::min(c->K, std::max(Hr, 1)) + T * c->S;
+    rows = (int)std::min<uint64_t>(legs + (uint64_t)H * kRowAlign, 0x7fffffff);
+  }
+  rows = (int)al((uint64_t)rows, kRowAlign);
+  uint64_t o = 0;
+  auto take = [&](uint64_t bytes, uint64_t a = 256) { o = al(o, a); uint64_t r = o; o += bytes; return r; };
+  L->err = take(64);
+  L->stats = take(64, 64);
+  L->done = take(64, 64);
+  L->cctr = take(64, 64);
+  L->qctr = take((uint64_t)c->L * H * 16, 64);     // snapshot = [0, qctr end)
+  L->rings = take((uint64_t)c->L * H * rc * 16);
+  L->cring = take((uint64_t)crc * 16);
+  L->cinfo = take(16);
+  L->h = take(T * d * es);
+  L->x = take(T * d * es);
+  L->pool = take(T * KS * d * es);
+  L->legs_done = take(T * 4);
+  L->tok_layer = take(T * 4);
+  L->tok_pass = take(T * 4);
+  L->tok_w = take(T * c->K * 4);
+  L->tok_idx = take(T * c->K * 4);
+  L->wmaps = take((uint64_t)c->L * H * 3 * 128, 128);
+  L->wptrs = take((uint64_t)c->L * H * 3 * 8);
+  L->s_qinfo = take(3 * AMOE_MAX_GROUP * 4);
+  L->s_meta = take((uint64_t)rows * 16);
+  L->s_tile = take((uint64_t)rows * d * es, 1024);
+  L->s_act = take((uint64_t)rows * ff * es, 1024);
+  L->s_out = take((uint64_t)rows * d * es, 1024);
+  L->total = al(o, 256);
+  L->rows_cap = rows;
+  *Hr_out = Hr;
+  *ring_cap = rc;
+  *cring_cap = crc;
+}
+
+#define CK(x)                                   \
+  do {                                          \
+    if ((x) != cudaSuccess) return AMOE_ECUDA;  \
+  } while (0)
+
+extern "C" {
+
+size_t amoe_workspace_bytes(const amoe_config* cfg) {
+  if (!valid_cfg(cfg)) return 0;
+  Layout L;
+  int Hr;
+  uint32_t rc, crc;
+  compute_layout(cfg, &L, &Hr, &rc, &crc);
+  return (size_t)L.total;
+}
+
+const char* amoe_status_string(amoe_status s) {
+  switch (s) {
+    case AMOE_OK: return "ok";
+    case AMOE_IDLE: return "idle: all hosted queues empty";
+    case AMOE_EINVAL: return "invalid argument";
+    case AMOE_ENOTHOSTED: return "expert not hosted on this rank";
+    case AMOE_ECUDA: return "CUDA runtime error";
+    case AMOE_EDEVICE: return "device-side invariant breach (see amoe_error_info)";
+    case AMOE_EPEER: return "peer workspaces missing or inconsistent";
+    case AMOE_ENOMEM: return "workspace too small";
+  }
+  return "unknown status";
+}
+
+amoe_status amoe_create(const amoe_config* cfg, void* workspace, size_t bytes, amoe_ctx_t* out) {
+  if (!valid_cfg(cfg) || !workspace || !out || (reinterpret_cast<uintptr_t>(workspace) & 255)) return AMOE_EINVAL;
+  amoe_ctx* c = new amoe_ctx();
+  c->cfg = *cfg;
+  uint32_t rc, crc;
+  compute_layout(cfg, &c->lay, &c->Hr, &rc, &crc);
+  if (bytes < c->lay.total) { delete c; return AMOE_ENOMEM; }
+  c->H = c->Hr + cfg->S;
+  c->ws = static_cast<char*>(workspace);
+  c->ws_bytes = bytes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  DevCtx& d = c->dc;
+  memset(&d, 0, sizeof(d));
+  d.L = cfg->L; d.E = cfg->E; d.K = cfg->K; d.S = cfg->S; d.d = cfg->d; d.ff = cfg->ff;
+  d.G = cfg->G; d.rank = cfg->rank; d.T = cfg->T_slots; d.dtype = cfg->dtype;
+  d.H = c->H; d.Hr = c->Hr; d.KS = cfg->K + cfg->S; d.esize = cfg->dtype == AMOE_BF16 ? 2 : 4;
+  d.ring_cap = rc; d.ring_mask = rc - 1; d.cring_cap = crc; d.cring_mask = crc - 1;
+  d.eps = cfg->rms_eps > 0.f ? cfg->rms_eps : 1e-6f;
+  d.n_tab = 0; d.router = nullptr;
+  d.lay = c->lay;
+  int owner[AMOE_MAX_E];
+  resolve_owner(cfg, owner);
+  int cnt[AMOE_MAX_G] = {0};
+  for (int e = 0; e < cfg->E; ++e) { d.owner[e] = (uint8_t)owner[e]; d.lq[e] = (int16_t)cnt[owner[e]]++; }
+  for (int r = 0; r < AMOE_MAX_G; ++r) d.peer[r] = 0;
+  d.peer[cfg->rank] = reinterpret_cast<uint64_t>(workspace);
+  c->hosted_flags.assign((size_t)cfg->L * c->H, 0);
+  c->wptrs.assign((size_t)cfg->L * c->H * 3, 0);
+  c->snap_bytes = c->lay.qctr + (uint64_t)cfg->L * c->H * 16;
+  if (cudaMallocHost(&c->pinned, c->snap_bytes) != cudaSuccess) { delete c; return AMOE_ECUDA; }
+  // zero counters, rings (seq flags) and token state; h/x/pool/scratch tiles need no init
+  if (cudaMemset(c->ws, 0, c->lay.h) != cudaSuccess ||
+      cudaMemset(c->ws + c->lay.legs_done, 0, c->lay.wmaps - c->lay.legs_done) != cudaSuccess ||
+      cudaMemset(c->ws + c->lay.wptrs, 0, c->lay.s_meta - c->lay.wptrs) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFreeHost(c->pinned);
+    delete c;
+    return AMOE_ECUDA;
+  }
+  c->launches = 0; c->admitted = 0; c->retired_base = 0; c->epoch = 0;
+  c->last_stream = 0;
+  *out = c;
+  return AMOE_OK;
+}
+
+amoe_status amoe_import_peers(amoe_ctx_t c, const uint64_t* peer_ws, int G) {
+  if (!c || !peer_ws || G != c->cfg.G) return AMOE_EINVAL;
+  if (peer_ws[c->cfg.rank] != reinterpret_cast<uint64_t>(c->ws)) return AMOE_EPEER;
+  for (int r = 0; r < G; ++r) {
+    if (!peer_ws[r] || (peer_ws[r] & 255)) return AMOE_EPEER;
+    c->dc.peer[r] = peer_ws[r];
+  }
+  return AMOE_OK;
+}
+
+int amoe_hosted(amoe_ctx_t c) { return c ? c->H : -1; }
+int amoe_ring_cap(amoe_ctx_t c) { return c ? (int)c->dc.ring_cap : -1; }
+int amoe_local_queue(amoe_ctx_t c, int e) {
+  if (!c || e < 0) return -1;
+  if (e < c->cfg.E) return c->dc.lq[e];
+  if (e < c->cfg.E + c->cfg.S) return c->Hr + (e - c->cfg.E);
+  return -1;
+}
+int64_t amoe_launch_count(amoe_ctx_t c) { return c ? c->launches : -1; }
+
+// queue slot (l*H + local) of (layer, expert) on THIS rank, or -1 if not hosted
+static int local_slot(amoe_ctx* c, int layer, int expert) {
+  if (layer < 0 || layer >= c->cfg.L) return -1;
+  if (expert >= 0 && expert < c->cfg.E) {
+    if (c->dc.owner[expert] != c->cfg.rank) return -1;
+    return layer * c->H + c->dc.lq[expert];
+  }
+  if (expert >= c->cfg.E && expert < c->cfg.E + c->cfg.S) return layer * c->H + c->Hr + (expert - c->cfg.E);
+  return -1;
+}
+
+amoe_status amoe_set_expert(amoe_ctx_t c, int layer, int expert, const void* w1, const void* w3, const void* w2) {
+  if (!c || !w1 || !w3 || !w2) return AMOE_EINVAL;
+  if (layer < 0 || layer >= c->cfg.L || expert < 0 || expert >= c->cfg.E + c->cfg.S) return AMOE_EINVAL;
+  const int slot = local_slot(c, layer, expert);
+  if (slot < 0) return AMOE_ENOTHOSTED;
+  for (const void* p : {w1, w3, w2})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return AMOE_EINVAL;
+  uint64_t ptrs[3] = {reinterpret_cast<uint64_t>(w1), reinterpret_cast<uint64_t>(w3), reinterpret_cast<uint64_t>(w2)};
+  CK(cudaMemcpy(c->ws + c->lay.wptrs + (uint64_t)slot * 24, ptrs, 24, cudaMemcpyHostToDevice));
+  if (c->cfg.dtype == AMOE_BF16) {
+    CUtensorMap maps[3];
+    const int bn = (c->cfg.d % 256 == 0) ? 256 : 128;
+    if (!encode_bf16_2d(&maps[0], w1, c->cfg.ff, c->cfg.d, 128) ||
+        !encode_bf16_2d(&maps[1], w3, c->cfg.ff, c->cfg.d, 128) ||
+        !encode_bf16_2d(&maps[2], w2, c->cfg.d, c->cfg.ff, bn))
+      return AMOE_ECUDA;
+    CK(cudaMemcpy(c->ws + c->lay.wmaps + (uint64_t)slot * 3 * 128, maps, sizeof(maps), cudaMemcpyHostToDevice));
+  }
+  for (int i = 0; i < 3; ++i) c->wptrs[(size_t)slot * 3 + i] = ptrs[i];
+  c->hosted_flags[slot] = 1;
+  return AMOE_OK;
+}
+
+amoe_status amoe_set_router(amoe_ctx_t c, const float* table, int n_tables) {
+  if (!c || !table || n_tables < 1) return AMOE_EINVAL;
+  c->dc.router = table;
+  c->dc.n_tab = n_tables;
+  return AMOE_OK;
+}
+
+amoe_status amoe_token_init(amoe_ctx_t c, const int32_t* slots, int T, const void* h0, int pass, void* stream) {
+  if (!c || T < 0 || (T > 0 && (!slots || !h0))) return AMOE_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches += launch_token_init(c->dc, slots, T, h0, pass, s);
+  c->admitted += T;
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
+amoe_status amoe_enqueue(amoe_ctx_t c, int layer, const int32_t* slots, int T, const float* logits,
+                         const int32_t* topk_idx, const float* topk_w, void* stream) {
+  if (!c || T < 0 || layer < 0 || layer >= c->cfg.L) return AMOE_EINVAL;
+  if (T > 0 && (!slots || (!logits && (!topk_idx || !topk_w)))) return AMOE_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int r = 0; r < c->cfg.G; ++r)
+    if (!c->dc.peer[r]) return AMOE_EPEER;
+  c->launches += launch_enqueue(c->dc, layer, slots, T, logits, topk_idx, topk_w, s);
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
+static amoe_status snapshot(amoe_ctx* c, cudaStream_t s) {
+  CK(cudaMemcpyAsync(c->pinned, c->ws, c->snap_bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return AMOE_OK;
+}
+
+static void depths_from_snapshot(amoe_ctx* c, uint32_t* Q) {
+  const uint32_t* q = c->pinned + c->lay.qctr / 4;
+  const int n = c->cfg.L * c->H;
+  for (int i = 0; i < n; ++i) Q[i] = q[4 * i + 1] - q[4 * i + 2];
+}
+
+amoe_status amoe_queue_depths(amoe_ctx_t c, uint32_t* host_out, void* stream) {
+  if (!c || !host_out) return AMOE_EINVAL;
+  amoe_status st = snapshot(c, (cudaStream_t)stream);
+  if (st != AMOE_OK) return st;
+  depths_from_snapshot(c, host_out);
+  return AMOE_OK;
+}
+
+amoe_status amoe_pick(amoe_ctx_t c, const uint32_t* Q, int policy, int W, float delta, int* layer, int* queue) {
+  if (!c || !Q || !layer || !queue || policy < 0 || policy > 2 || W < 0) return AMOE_EINVAL;
+  return pick_queue(Q, c->cfg.L, c->H, c->cfg.E + c->cfg.S, policy, W, (double)delta, layer, queue) ? AMOE_IDLE
+                                                                                                   : AMOE_OK;
+}
+
+amoe_status amoe_schedule(const uint32_t* Q, int n_blocks, int n_queues, int n_experts, int policy, int W,
+                          float delta, int* block, int* queue) {
+  if (!Q || !block || !queue || n_blocks < 1 || n_queues < 1 || n_experts < 1 || policy < 0 || policy > 2 || W < 0)
+    return AMOE_EINVAL;
+  return pick_queue(Q, n_blocks, n_queues, n_experts, policy, W, (double)delta, block, queue) ? AMOE_IDLE : AMOE_OK;
+}
+
+static amoe_status make_group(amoe_ctx* c, const amoe_group* g, int max_tokens, GroupDev* gd, int* wslot) {
+  if (!g || g->nq < 1 || g->nq > AMOE_MAX_GROUP || g->rows_cap < kRowAlign || !g->tile || !g->meta || !g->qinfo)
+    return AMOE_EINVAL;
+  memset(gd, 0, sizeof(*gd));
+  gd->nq = g->nq;
+  gd->rows_cap = g->rows_cap;
+  gd->max_tokens = max_tokens > 0 ? max_tokens : 0;
+  if (c->cfg.max_batch > 0 && (gd->max_tokens == 0 || gd->max_tokens > c->cfg.max_batch)) gd->max_tokens = c->cfg.max_batch;
+  gd->qinfo = g->qinfo;
+  gd->meta = g->meta;
+  gd->tile = g->tile;
+  gd->out = g->out;
+  for (int q = 0; q < g->nq; ++q) {
+    const int slot = local_slot(c, g->layer[q], g->expert[q]);
+    if (slot < 0) return AMOE_ENOTHOSTED;
+    for (int p = 0; p < q; ++p)
+      if (gd->qid[p] == slot) return AMOE_EINVAL;   // a queue may appear once per group
+    gd->qid[q] = slot;
+    if (wslot) wslot[q] = slot * 3;
+  }
+  return AMOE_OK;
+}
+
+amoe_status amoe_rebatch(amoe_ctx_t c, const amoe_group* g, int max_tokens, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  GroupDev gd;
+  amoe_status st = make_group(c, g, max_tokens, &gd, nullptr);
+  if (st != AMOE_OK) return st;
+  for (int r = 0; r < c->cfg.G; ++r)
+    if (!c->dc.peer[r]) return AMOE_EPEER;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches += launch_drain(c->dc, gd, s);
+  c->launches += launch_gather(c->dc, gd, c->num_sms, s);
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
+amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  GroupDev gd;
+  int wslot[AMOE_MAX_GROUP];
+  amoe_status st = make_group(c, g, 0, &gd, wslot);
+  if (st != AMOE_OK) return st;
+  if (!g->act || !g->out) return AMOE_EINVAL;
+  for (int q = 0; q < g->nq; ++q)
+    if (!c->hosted_flags[wslot[q] / 3]) return AMOE_EINVAL;   // weights not registered
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->cfg.dtype == AMOE_BF16) {
+    const CUtensorMap* mt = cached_map(c, g->tile, g->rows_cap, c->cfg.d, 128);
+    const CUtensorMap* ma = cached_map(c, g->act, g->rows_cap, c->cfg.ff, 128);
+    if (!mt || !ma) return AMOE_ECUDA;
+    FfnLaunch f;
+    f.nq = g->nq;
+    f.qinfo = g->qinfo;
+    f.wmaps = reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps);
+    for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
+    c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, c->num_sms, s);
+  } else {
+    c->launches += launch_ffn_simt(c->dc, g->nq, g->qinfo, wslot, reinterpret_cast<const uint64_t*>(c->ws + c->lay.wptrs),
+                                   g->tile, g->act, g->out, c->num_sms, s);
+  }
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
+amoe_status amoe_forward(amoe_ctx_t c, const amoe_group* g, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  GroupDev gd;
+  amoe_status st = make_group(c, g, 0, &gd, nullptr);
+  if (st != AMOE_OK) return st;
+  if (!g->out) return AMOE_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches += launch_forward(c->dc, gd, c->num_sms, s);
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
+amoe_status amoe_combine(amoe_ctx_t c, int retire_pass, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevCtx dc = c->dc;
+  if (!dc.router) { dc.n_tab = 1; }
+  c->launches += launch_combine(dc, retire_pass, s);
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
+amoe_status amoe_scratch_group(amoe_ctx_t c, amoe_group* g) {
+  if (!c || !g) return AMOE_EINVAL;
+  memset(g, 0, sizeof(*g));
+  g->rows_cap = c->lay.rows_cap;
+  g->tile = c->ws + c->lay.s_tile;
+  g->meta = reinterpret_cast<amoe_leg*>(c->ws + c->lay.s_meta);
+  g->qinfo = reinterpret_cast<int32_t*>(c->ws + c->lay.s_qinfo);
+  g->act = c->ws + c->lay.s_act;
+  g->out = c->ws + c->lay.s_out;
+  return AMOE_OK;
+}
+
+amoe_status amoe_check(amoe_ctx_t c) {
+  if (!c) return AMOE_EINVAL;
+  CK(cudaDeviceSynchronize());
+  uint32_t e = 0;
+  CK(cudaMemcpy(&e, c->ws + c->lay.err, 4, cudaMemcpyDeviceToHost));
+  return e ? AMOE_EDEVICE : AMOE_OK;
+}
+
+amoe_status amoe_error_info(amoe_ctx_t c, uint32_t info[4]) {
+  if (!c || !info) return AMOE_EINVAL;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(info, c->ws + c->lay.err, 16, cudaMemcpyDeviceToHost));
+  return AMOE_OK;
+}
+
+amoe_status amoe_clear_error(amoe_ctx_t c) {
+  if (!c) return AMOE_EINVAL;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemset(c->ws + c->lay.err, 0, 16));
+  return AMOE_OK;
+}
+
+amoe_status amoe_get_buffer(amoe_ctx_t c, int which, void** ptr, size_t* bytes) {
+  if (!c || !ptr || !bytes) return AMOE_EINVAL;
+  const uint64_t T = c->cfg.T_slots, d = c->cfg.d, es = c->dc.esize, KS = c->dc.KS, K = c->cfg.K;
+  uint64_t off, n;
+  switch (which) {
+    case AMOE_BUF_H: off = c->lay.h; n = T * d * es; break;
+    case AMOE_BUF_X: off = c->lay.x; n = T * d * es; break;
+    case AMOE_BUF_POOL: off = c->lay.pool; n = T * KS * d * es; break;
+    case AMOE_BUF_TOK_W: off = c->lay.tok_w; n = T * K * 4; break;
+    case AMOE_BUF_TOK_IDX: off = c->lay.tok_idx; n = T * K * 4; break;
+    case AMOE_BUF_TOK_LAYER: off = c->lay.tok_layer; n = T * 4; break;
+    case AMOE_BUF_TOK_PASS: off = c->lay.tok_pass; n = T * 4; break;
+    case AMOE_BUF_RINGS: off = c->lay.rings; n = (uint64_t)c->cfg.L * c->H * c->dc.ring_cap * 16; break;
+    case AMOE_BUF_QCTR: off = c->lay.qctr; n = (uint64_t)c->cfg.L * c->H * 16; break;
+    case AMOE_BUF_STATS: off = c->lay.stats; n = 64; break;
+    case AMOE_BUF_SCRATCH: off = c->lay.s_tile; n = c->lay.total - c->lay.s_tile; break;
+    default: return AMOE_EINVAL;
+  }
+  *ptr = c->ws + off;
+  *bytes = n;
+  return AMOE_OK;
+}
+
+amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, amoe_run_stats* stats, void* stream) {
+  if (!c || !p || p->policy < 0 || p->policy > 2 || p->W < 0) return AMOE_EINVAL;
+  for (int r = 0; r < c->cfg.G; ++r)
+    if (!c->dc.peer[r]) return AMOE_EPEER;
+  if (!c->dc.router) return AMOE_EINVAL;
+  for (size_t i = 0; i < c->hosted_flags.size(); ++i)
+    if (!c->hosted_flags[i]) {
+      // every hosted queue needs weights (routed experts of this rank and the shared experts)
+      const int q = (int)(i % c->H);
+      if (q < c->Hr) {
+        bool exists = false;
+        for (int e = 0; e < c->cfg.E; ++e) exists |= (c->dc.owner[e] == c->cfg.rank && c->dc.lq[e] == q);
+        if (!exists) continue;
+      }
+      return AMOE_EINVAL;
+    }
+  cudaStream_t s = (cudaStream_t)stream;
+  c->last_stream = s;
+  amoe_run_stats rs{};
+  const uint32_t epoch = ++c->epoch;
+  const int64_t expected = c->admitted;
+  c->admitted = 0;
+  amoe_group g;
+  amoe_scratch_group(c, &g);
+  const int L = c->cfg.L, H = c->H;
+  std::vector<uint32_t> Q((size_t)L * H);
+  amoe_status st = snapshot(c, s);
+  if (st != AMOE_OK) return st;
+  const uint64_t* s0 = reinterpret_cast<const uint64_t*>(reinterpret_cast<const char*>(c->pinned) + c->lay.stats);
+  const uint64_t retired0 = s0[1], merged0 = s0[0], legs0 = s0[2];
+  bool announced = false;
+  int idle_streak = 0;
+  for (;;) {
+    st = snapshot(c, s);
+    if (st != AMOE_OK) return st;
+    const char* snap = reinterpret_cast<const char*>(c->pinned);
+    if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return AMOE_EDEVICE;
+    const uint64_t* sv = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
+    if (!announced && (int64_t)(sv[1] - retired0) >= expected) {
+      c->launches += launch_announce(c->dc, epoch, s);
+      rs.kernel_launches += 1;
+      announced = true;
+      continue;
+    }
+    if (announced) {
+      const uint32_t* done = reinterpret_cast<const uint32_t*>(snap + c->lay.done);
+      bool all = true;
+      for (int r = 0; r < c->cfg.G; ++r) all &= done[r] == epoch;
+      if (all) {
+        rs.token_layers = (int64_t)(sv[0] - merged0);
+        rs.legs = (int64_t)(sv[2] - legs0);
+        break;
+      }
+    }
+    depths_from_snapshot(c, Q.data());
+    const uint32_t* cc = reinterpret_cast<const uint32_t*>(snap + c->lay.cctr);
+    const uint32_t cpend = cc[1] - cc[2];
+    int b = -1, q = -1;
+    const bool work = pick_queue(Q.data(), L, H, c->cfg.E + c->cfg.S, p->policy, p->W, (double)p->delta, &b, &q) == 0;
+    if (work) {
+      g.nq = 0;
+      if (p->grouped) {
+        for (int j = 0; j < H && g.nq < AMOE_MAX_GROUP; ++j)
+          if (Q[(size_t)b * H + j] > 0) {
+            g.layer[g.nq] = b;
+            g.expert[g.nq] = j < c->Hr ? -1 : c->cfg.E + (j - c->Hr);
+            if (j < c->Hr)
+              for (int e = 0; e < c->cfg.E; ++e)
+                if (c->dc.owner[e] == c->cfg.rank && c->dc.lq[e] == j) g.expert[g.nq] = e;
+            ++g.nq;
+          }
+      } else {
+        g.layer[0] = b;
+        g.expert[0] = q < c->Hr ? -1 : c->cfg.E + (q - c->Hr);
+        if (q < c->Hr)
+          for (int e = 0; e < c->cfg.E; ++e)
+            if (c->dc.owner[e] == c->cfg.rank && c->dc.lq[e] == q) g.expert[0] = e;
+        g.nq = 1;
+      }
+      const int64_t l0 = c->launches;
+      if ((st = amoe_rebatch(c, &g, 0, s)) != AMOE_OK) return st;
+      if ((st = amoe_expert_ffn(c, &g, s)) != AMOE_OK) return st;
+      if ((st = amoe_forward(c, &g, s)) != AMOE_OK) return st;
+      if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
+      rs.kernel_launches += c->launches - l0;
+      rs.picks += 1;
+      rs.queues_run += g.nq;
+      idle_streak = 0;
+    } else if (cpend > 0) {
+      const int64_t l0 = c->launches;
+      if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
+      rs.kernel_launches += c->launches - l0;
+      idle_streak = 0;
+    } else {
+      rs.idle_polls += 1;
+      if (c->cfg.G == 1 && !announced) {
+        // single GPU: nothing queued and tokens not retired means a lost leg
+        rs.token_layers = (int64_t)(sv[0] - merged0);
+        if (stats) *stats = rs;
+        return AMOE_EDEVICE;
+      }
+      if (++idle_streak > 64) std::this_thread::sleep_for(std::chrono::microseconds(5));
+    }
+    if (p->max_picks > 0 && rs.picks >= p->max_picks) break;
+  }
+  if (stats) *stats = rs;
+  return AMOE_OK;
+}
+
+amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, void* h_out_host, int pass, const amoe_run_params* p,
+                           amoe_run_stats* stats, void* stream) {
+  if (!c || !h0_host || !h_out_host || !p || !c->dc.router) return AMOE_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)c->cfg.T_slots * c->cfg.d * c->dc.esize;
+  // all slots, identity order: the slot list lives in the scratch meta area head (int32 iota)
+  static_assert(sizeof(amoe_leg) == 16, "leg layout");
+  int32_t* slots = reinterpret_cast<int32_t*>(c->ws + c->lay.s_meta);
+  if ((uint64_t)c->lay.rows_cap * 16 < (uint64_t)c->cfg.T_slots * 4) return AMOE_EINVAL;
+  std::vector<int32_t> iota(c->cfg.T_slots);
+  for (int i = 0; i < c->cfg.T_slots; ++i) iota[i] = i;
+  CK(cudaMemcpyAsync(slots, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->ws + c->lay.h, h0_host, bytes, cudaMemcpyHostToDevice, s));
+  amoe_status st = amoe_token_init(c, slots, c->cfg.T_slots, c->ws + c->lay.h, pass, s);
+  if (st != AMOE_OK) return st;
+  const float* z0 = c->dc.router + (uint64_t)(pass % c->dc.n_tab) * c->cfg.L * c->cfg.T_slots * c->cfg.E;
+  if ((st = amoe_enqueue(c, 0, slots, c->cfg.T_slots, z0, nullptr, nullptr, s)) != AMOE_OK) return st;
+  CK(cudaStreamSynchronize(s));   // the slot list area is reused as scratch by amoe_run
+  if ((st = amoe_run(c, p, pass + 1, stats, s)) != AMOE_OK) return st;
+  CK(cudaMemcpyAsync(h_out_host, c->ws + c->lay.h, bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return AMOE_OK;
+}
+
+amoe_status amoe_destroy(amoe_ctx_t c) {
+  if (!c) return AMOE_EINVAL;
+  if (c->pinned) cudaFreeHost(c->pinned);
+  delete c;
+  return AMOE_OK;
+}
+
+}  // extern "C"

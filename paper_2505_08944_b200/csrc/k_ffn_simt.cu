@@ -1,0 +1,120 @@
+// k_ffn_simt.cu — a5/a6 in the fp32 mode (BASELINE.json: "1e-5 in an fp32 mode").
+// tcgen05 has no fp32-input kind (kind::tf32 keeps a 10-bit mantissa), so the exact mode runs on
+// the FP32 pipes: 64x64 output tiles, 4x4 per thread, K staged through shared memory in slices
+// of 16, two-level accumulation (a partial sum per 64-wide K block added into the total) so the
+// rounding error grows with K/64 + 64 instead of K (a serial fp32 sum over
+// K = 14336 has only 1.4x margin to 1e-5). Persistent over every queue of a grouped pick.
+#include "amoe_internal.cuh"
+
+namespace amoe {
+namespace simt {
+
+constexpr int TM = 64, TN = 64, TK = 16, THREADS = 256;
+
+struct SimtArgs {
+  int32_t nq;
+  int32_t mode;          // 0 gate/up (+SwiGLU), 1 down
+  int32_t N;             // output columns (ff or d)
+  int32_t Kd;            // reduction length (d or ff)
+  const int32_t* qinfo;
+  const uint64_t* wptrs; // [L*H][3] device pointers
+  const float* in;       // tile (mode 0) or act (mode 1), row stride Kd
+  float* out;            // act (mode 0) or out (mode 1), row stride N
+  int32_t wslot[AMOE_MAX_GROUP];
+};
+
+__global__ void __launch_bounds__(THREADS) ffn_simt_kernel(SimtArgs a) {
+  __shared__ float As[TK][TM + 1];
+  __shared__ float Bs[TK][TN + 1];
+  __shared__ float Cs[TK][TN + 1];
+  __shared__ int s_n[AMOE_MAX_GROUP], s_off[AMOE_MAX_GROUP], s_pre[AMOE_MAX_GROUP + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int ntn = a.N / TN;
+  if (tid == 0) {
+    int acc = 0;
+    for (int q = 0; q < a.nq; ++q) {
+      s_n[q] = a.qinfo[q]; s_off[q] = a.qinfo[AMOE_MAX_GROUP + q];
+      s_pre[q] = acc; acc += (s_n[q] + TM - 1) / TM * ntn;
+    }
+    s_pre[a.nq] = acc;
+  }
+  __syncthreads();
+  const int total = s_pre[a.nq];
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    int q = 0;
+    while (q + 1 < a.nq && s_pre[q + 1] <= t) ++q;
+    const int u = t - s_pre[q];
+    const int mt = u / ntn, nt = u % ntn;
+    const float* W = reinterpret_cast<const float*>(a.wptrs[a.wslot[q] + (a.mode == 0 ? 0 : 2)]);
+    const float* W3 = reinterpret_cast<const float*>(a.wptrs[a.wslot[q] + 1]);
+    const int row0 = mt * TM, col0 = nt * TN;
+    const int nrow = s_n[q];
+    const float* A = a.in + (uint64_t)s_off[q] * a.Kd;
+    float acc[4][4] = {}, acc3[4][4] = {}, part[4][4] = {}, part3[4][4] = {};
+    for (int k0 = 0; k0 < a.Kd; k0 += TK) {
+      // load A [64 x 16], B [64 x 16] (and W3) transposed into smem
+      for (int i = tid; i < TM * TK; i += THREADS) {
+        const int r = i / TK, kk = i % TK;
+        const int gr = row0 + r;
+        As[kk][r] = gr < nrow ? A[(uint64_t)gr * a.Kd + k0 + kk] : 0.f;
+        Bs[kk][r] = W[(uint64_t)(col0 + r) * a.Kd + k0 + kk];
+        if (a.mode == 0) Cs[kk][r] = W3[(uint64_t)(col0 + r) * a.Kd + k0 + kk];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        float av[4], bv[4], cv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty * 4 + i]; bv[i] = Bs[kk][tx * 4 + i]; cv[i] = Cs[kk][tx * 4 + i]; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            part[i][j] = fmaf(av[i], bv[j], part[i][j]);
+            if (a.mode == 0) part3[i][j] = fmaf(av[i], cv[j], part3[i][j]);
+          }
+      }
+      __syncthreads();
+      if (((k0 + TK) & 63) == 0 || k0 + TK >= a.Kd) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[i][j] += part[i][j]; part[i][j] = 0.f;
+            acc3[i][j] += part3[i][j]; part3[i][j] = 0.f;
+          }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gr = row0 + ty * 4 + i;
+      if (gr >= nrow) continue;
+      float* orow = a.out + (uint64_t)(s_off[q] + gr) * a.N + col0 + tx * 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float g = acc[i][j];
+        orow[j] = a.mode == 0 ? g / (1.0f + expf(-g)) * acc3[i][j] : g;
+      }
+    }
+  }
+}
+
+}  // namespace simt
+
+int launch_ffn_simt(const DevCtx& c, int nq, const int32_t* qinfo, const int* wslot, const uint64_t* wptrs,
+                    const void* tile, void* act, void* out, int num_sms, cudaStream_t s) {
+  simt::SimtArgs a{};
+  a.nq = nq;
+  a.qinfo = qinfo;
+  a.wptrs = wptrs;
+  for (int q = 0; q < nq; ++q) a.wslot[q] = wslot[q];
+  a.mode = 0; a.N = c.ff; a.Kd = c.d;
+  a.in = (const float*)tile; a.out = (float*)act;
+  simt::ffn_simt_kernel<<<num_sms * 4, simt::THREADS, 0, s>>>(a);
+  a.mode = 1; a.N = c.d; a.Kd = c.ff;
+  a.in = (const float*)act; a.out = (float*)out;
+  simt::ffn_simt_kernel<<<num_sms * 4, simt::THREADS, 0, s>>>(a);
+  return 2;
+}
+
+}  // namespace amoe

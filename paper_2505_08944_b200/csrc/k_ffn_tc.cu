@@ -1,0 +1,332 @@
+// k_ffn_tc.cu — a5/a6: grouped expert FFN on the 5th-generation tensor cores (sm_100a).
+//
+// One persistent, warp-specialised kernel per GEMM of the SwiGLU expert
+// (reading c1: O = W2 (silu(W1 x) ⊙ W3 x)), covering every queue of a grouped pick:
+//   MODE_GATEUP: D[128 x 256] = X_tile[128 x d] · [W1 rows n0..n0+127 ; W3 rows n0..n0+127]ᵀ,
+//                epilogue act = bf16(silu(D[:, :128]) ⊙ D[:, 128:])       (SwiGLU fused)
+//   MODE_DOWN  : D[128 x BN] = act_tile[128 x ff] · W2[n0..n0+BN-1, :]ᵀ, epilogue out = bf16(D)
+// Warp roles (256 threads): warp 0 = TMA producer, warp 1 = tcgen05.mma issuer (one thread),
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM -> registers -> global).
+// Operands: TMA 2D tiles, 128-byte swizzle, K-major; 4-stage smem ring (48 KB/stage) with
+// full/empty mbarriers; two 256-column fp32 accumulators in TMEM so the epilogue of tile i
+// overlaps the main loop of tile i+1. Tiles of a queue are rasterised in groups of 16 M-tiles
+// so concurrently running CTAs share the weight slab and the token rows through L2.
+#include "amoe_internal.cuh"
+
+namespace amoe {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle atom row
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KB
+constexpr int B_BYTES = 256 * BK * 2;           // 32 KB (max BN = 256)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 256;
+constexpr int GROUP_M = 16;
+constexpr int TMEM_COLS = 512;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;   // + barriers/tile tables + align
+
+enum Mode { MODE_GATEUP = 0, MODE_DOWN = 1 };
+
+struct FfnArgs {
+  int32_t nq;
+  int32_t n_tiles;       // N tiles per queue
+  int32_t k_blocks;      // K / 64
+  int32_t out_ld;        // output row stride (elements)
+  int32_t out_cols;      // valid output columns
+  int32_t w_which;       // 0 (W1; W3 = +1) or 2 (W2) within a queue's 3 tensor maps
+  const int32_t* qinfo;
+  const CUtensorMap* wmaps;
+  __nv_bfloat16* out;
+  int32_t wslot[AMOE_MAX_GROUP];   // (l*H + lq) * 3
+};
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" :: "r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" :: "l"(tmap) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major operand with 128-byte swizzle: 8-row core groups of
+// 1024 B (SBO = 1024), LBO unused for swizzled K-major (1), version 1 (sm_100), layout 2.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(bar) : "memory");
+}
+// 32 lanes x 32 columns of fp32 accumulator -> 32 registers per thread (thread i = lane i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ tile schedule
+struct Sched {
+  int nq, n_tiles, total;
+  const int* n;
+  const int* off;
+  const int* pre;     // tile prefix per queue
+  __device__ __forceinline__ void decode(int t, int& q, int& m, int& nb) const {
+    int lo = 0, hi = nq - 1;
+    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (pre[mid] <= t) lo = mid; else hi = mid - 1; }
+    q = lo;
+    const int u = t - pre[q];
+    const int m_tiles = (n[q] + BM - 1) / BM;
+    const int gsz = GROUP_M * n_tiles;
+    const int g = u / gsz;
+    const int first_m = g * GROUP_M;
+    const int gm = min(m_tiles - first_m, GROUP_M);
+    const int r = u - g * gsz;
+    m = first_m + r % gm;
+    nb = r / gm;
+  }
+};
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
+
+template <int MODE, int BN>
+__global__ void __launch_bounds__(THREADS, 1)
+ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* tiles = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  int* s_n = reinterpret_cast<int*>(tmem_holder + 4);
+  int* s_off = s_n + AMOE_MAX_GROUP;
+  int* s_pre = s_off + AMOE_MAX_GROUP;   // AMOE_MAX_GROUP + 1
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nq = args.nq;
+  for (int q = tid; q < nq; q += THREADS) { s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BM - 1) / BM * args.n_tiles; }
+    s_pre[nq] = acc;
+    for (int s = 0; s < STAGES; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES + s]), 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(smem_u32(&bars[2 * STAGES + a]), 1); mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch(&tmA);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_holder)), "r"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  Sched sc{nq, args.n_tiles, s_pre[nq], s_n, s_off, s_pre};
+  const int kb_n = args.k_blocks;
+
+  if (warp == 0 && lane == 0) {
+    // ===================== TMA producer
+    int stage = 0; uint32_t phase = 0;
+    for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+      int q, m, nb;
+      sc.decode(t, q, m, nb);
+      const int arow = s_off[q] + m * BM;
+      const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
+      for (int kb = 0; kb < kb_n; ++kb) {
+        mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
+        const uint32_t full = smem_u32(&bars[stage]);
+        const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
+        const uint32_t sb = sa + A_BYTES;
+        mbar_expect_tx(full, A_BYTES + BN * BK * 2);
+        tma_load_2d(sa, &tmA, kb * BK, arow, full);
+        if (MODE == MODE_GATEUP) {
+          tma_load_2d(sb, wb, kb * BK, nb * 128, full);
+          tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
+        } else {
+          tma_load_2d(sb, wb, kb * BK, nb * BN, full);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===================== MMA issuer (single thread)
+    constexpr uint32_t idesc = idesc_bf16(BM, BN);
+    int stage = 0; uint32_t phase = 0;
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+      mbar_wait(smem_u32(&bars[2 * STAGES + 2 + acc]), acc_phase ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+      for (int kb = 0; kb < kb_n; ++kb) {
+        mbar_wait(smem_u32(&bars[stage]), phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
+        const uint64_t adesc = umma_desc_sw128(sa);
+        const uint64_t bdesc = umma_desc_sw128(sa + A_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the swizzle atom = +2 in desc units
+          umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+        umma_commit(smem_u32(&bars[STAGES + stage]));     // frees the smem stage when MMAs retire
+        if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+      }
+      umma_commit(smem_u32(&bars[2 * STAGES + acc]));      // accumulator ready
+      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> registers -> global
+    const int ew = warp - 4;            // TMEM lane quarter (warp % 4)
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+      int q, m, nb;
+      sc.decode(t, q, m, nb);
+      mbar_wait(smem_u32(&bars[2 * STAGES + acc]), acc_phase);
+      tc_fence_after();
+      const int row = m * BM + ew * 32 + lane;
+      const bool valid = row < s_n[q];
+      __nv_bfloat16* orow = args.out + (uint64_t)(s_off[q] + row) * args.out_ld;
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
+      if (MODE == MODE_GATEUP) {
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          float g[32], u[32];
+          tmem_ld32(taddr + ch * 32, g);
+          tmem_ld32(taddr + 128 + ch * 32, u);
+          if (valid) {
+            uint4 pk[4];
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              p2[j] = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
+            uint4* dst = reinterpret_cast<uint4*>(orow + nb * 128 + ch * 32);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          float v[32];
+          tmem_ld32(taddr + ch * 32, v);
+          const int col = nb * BN + ch * 32;
+          if (valid && col < args.out_cols) {
+            uint4 pk[4];
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) p2[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+            uint4* dst = reinterpret_cast<uint4*>(orow + col);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&bars[2 * STAGES + 2 + acc]));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------ launchers
+
+
+int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_tile, const CUtensorMap& tm_act,
+                  void* act, void* out, int num_sms, cudaStream_t s) {
+  using namespace tc;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(ffn_tc_kernel<MODE_GATEUP, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(ffn_tc_kernel<MODE_DOWN, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(ffn_tc_kernel<MODE_DOWN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_done = true;
+  }
+  FfnArgs a{};
+  a.nq = f.nq;
+  a.qinfo = f.qinfo;
+  a.wmaps = f.wmaps;
+  for (int q = 0; q < f.nq; ++q) a.wslot[q] = f.wslot[q];
+  // gate/up + SwiGLU: N tiles of 128 ff-columns (x2 for gate and up)
+  a.n_tiles = c.ff / 128;
+  a.k_blocks = c.d / BK;
+  a.out_ld = c.ff;
+  a.out_cols = c.ff;
+  a.w_which = 0;
+  a.out = reinterpret_cast<__nv_bfloat16*>(act);
+  ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a);
+  // down: N tiles of BN model columns
+  const int bn = (c.d % 256 == 0) ? 256 : 128;
+  a.n_tiles = c.d / bn;
+  a.k_blocks = c.ff / BK;
+  a.out_ld = c.d;
+  a.out_cols = c.d;
+  a.w_which = 2;
+  a.out = reinterpret_cast<__nv_bfloat16*>(out);
+  if (bn == 256) ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a);
+  else ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a);
+  return 2;
+}
+
+}  // namespace amoe

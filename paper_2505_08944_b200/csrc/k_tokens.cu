@@ -1,0 +1,370 @@
+// k_tokens.cu — token-side kernels of the AEP hot path (home rank):
+//   token_init  : admit tokens (h, x = rmsnorm(h), state)                     (reading c7)
+//   enqueue     : a1 router top-K + a2 scatter of the K legs into µ-queues
+//   cdrain      : snapshot of the combine ring (token pool readiness, L228)
+//   combine     : a8 weighted top-K merge + RMSNorm + relabel + fused a1/a2     (L175, L209, L228, L236)
+//   announce    : multi-GPU quiescence flag
+#include "amoe_internal.cuh"
+
+namespace amoe {
+
+constexpr int kTokThreads = 256;
+constexpr int kTokWarps = kTokThreads / kWarp;
+constexpr int kTPW = 4;                       // tokens per warp per chunk
+constexpr int kTPC = kTokWarps * kTPW;        // tokens per CTA chunk
+
+struct PendingLeg {
+  int32_t r;      // owner rank (-1 = inactive)
+  int32_t q;      // queue index on the owner
+  amoe_leg g;
+};
+
+// ---------------------------------------------------------------------------- routing (a1)
+// Warp-cooperative top-K of z[0..E) (ties -> lower expert index) and softmax over the K
+// selected logits; every lane returns the same idx/w. fp32 expf (oracle: float64, |Δw| ≤ 1e-6).
+__device__ __forceinline__ void route_warp(const float* __restrict__ z, int E, int K, int lane,
+                                           int* idx, float* w) {
+  float v[AMOE_MAX_E / kWarp];
+  uint32_t chosen = 0;
+#pragma unroll
+  for (int j = 0; j < AMOE_MAX_E / kWarp; ++j) {
+    int e = lane + kWarp * j;
+    v[j] = e < E ? z[e] : -INFINITY;
+  }
+  float zs[kMaxKS];
+  for (int k = 0; k < K; ++k) {
+    float bv = -INFINITY;
+    int be = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < AMOE_MAX_E / kWarp; ++j) {
+      int e = lane + kWarp * j;
+      if (e < E && !((chosen >> j) & 1u) && (v[j] > bv || be == 0x7fffffff)) { bv = v[j]; be = e; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+    }
+    idx[k] = be;
+    zs[k] = bv;
+    if ((be & (kWarp - 1)) == lane) chosen |= 1u << (be / kWarp);
+  }
+  float s = 0.f;
+  float ex[kMaxKS];
+  for (int k = 0; k < K; ++k) { ex[k] = expf(zs[k] - zs[0]); s += ex[k]; }
+  for (int k = 0; k < K; ++k) w[k] = ex[k] / s;
+}
+
+// ---------------------------------------------------------------------------- scatter (a2)
+// Every thread of the CTA calls this. Legs with r >= 0 are appended to ring (r, q): one
+// reservation atomic per (warp, queue) (__match_any_sync aggregation), entries written with
+// the publication seq last, then one release-add of the commit counter per (warp, queue).
+// Remote rings use system-scope atomics over NVLink.
+__device__ void scatter_legs(const DevCtx& c, const PendingLeg* legs, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool active = i < n && legs[i].r >= 0;
+    const int r = active ? legs[i].r : 0;
+    const int q = active ? legs[i].q : 0;
+    const int key = active ? (r << 24 | q) : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    const bool sys = r != c.rank;
+    uint32_t pos0 = 0;
+    if (active && lane == leader) {
+      uint32_t* ctr = qctr_ptr(c, r, q);
+      pos0 = atom_add_relaxed(ctr, (uint32_t)__popc(peers), sys);
+      if (!sys) {
+        uint32_t head = ld_relaxed(ctr + 2);
+        if (pos0 + (uint32_t)__popc(peers) - head > c.ring_cap) raise_fault(c, F_RING_OVERFLOW, q, pos0, head);
+      }
+    }
+    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    if (active) {
+      const uint32_t pos = pos0 + __popc(peers & ((1u << lane) - 1u));
+      write_leg(ring_ptr(c, r, q), c.ring_mask, pos, legs[i].g, sys);
+    }
+    __syncwarp();
+    if (active && lane == leader) {
+      fence_sc(sys);
+      red_add_release(qctr_ptr(c, r, q) + 1, (uint32_t)__popc(peers), sys);
+    }
+  }
+}
+
+// Fill the K (+S) legs of one routed token (lanes < K+S write their own leg).
+__device__ __forceinline__ void make_legs(const DevCtx& c, int layer, int slot, const int* idx,
+                                          const float* w, int lane, PendingLeg* out) {
+  if (lane < c.K) {
+    const int e = idx[lane];
+    PendingLeg p;
+    if (e < 0 || e >= c.E) {
+      raise_fault(c, F_EXPERT_RANGE, slot, e, layer);
+      p.r = -1;
+    } else {
+      p.r = c.owner[e];
+      p.q = layer * c.H + c.lq[e];
+    }
+    p.g.token_slot = slot; p.g.k = (int16_t)lane; p.g.home = (int16_t)c.rank; p.g.w = w[lane]; p.g.seq = 0;
+    out[lane] = p;
+  } else if (lane < c.KS) {
+    PendingLeg p;
+    p.r = c.rank;
+    p.q = layer * c.H + c.Hr + (lane - c.K);
+    p.g.token_slot = slot; p.g.k = (int16_t)lane; p.g.home = (int16_t)c.rank; p.g.w = 1.0f; p.g.seq = 0;
+    out[lane] = p;
+  }
+}
+
+// ---------------------------------------------------------------------------- RMSNorm (c7)
+// x = store(h / sqrt(mean(h^2) + eps)) for one row held at `h` (storage T), warp-cooperative.
+template <typename T>
+__device__ __forceinline__ void rmsnorm_row(const DevCtx& c, const T* h, T* x, float ss, int lane) {
+  using V = Vec<T>;
+  const float r = 1.0f / sqrtf(ss / (float)c.d + c.eps);
+  for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
+    float f[V::N];
+    V::load(h + col, f);
+#pragma unroll
+    for (int j = 0; j < V::N; ++j) f[j] = f[j] * r;
+    V::store(x + col, f);
+  }
+}
+
+// ---------------------------------------------------------------------------- token_init
+
+template <typename T>
+__global__ void __launch_bounds__(kTokThreads) token_init_kernel(DevCtx c, const int32_t* __restrict__ slots,
+                                                                 int n, const T* __restrict__ h0, int pass) {
+  using V = Vec<T>;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < n; i += nw) {
+    const int slot = slots[i];
+    if (slot < 0 || slot >= c.T) { if (lane == 0) raise_fault(c, F_SLOT_RANGE, slot, c.T, 0); continue; }
+    T* h = wsp<T>(c, c.rank, c.lay.h) + (uint64_t)slot * c.d;
+    T* x = wsp<T>(c, c.rank, c.lay.x) + (uint64_t)slot * c.d;
+    const T* src = h0 + (uint64_t)i * c.d;
+    float ss = 0.f;
+    for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
+      float f[V::N];
+      V::load(src + col, f);
+      V::store(h + col, f);
+#pragma unroll
+      for (int j = 0; j < V::N; ++j) ss += f[j] * f[j];
+    }
+    ss = warp_sum(ss);
+    rmsnorm_row<T>(c, h, x, ss, lane);
+    if (lane == 0) {
+      wsp<int32_t>(c, c.rank, c.lay.tok_layer)[slot] = 0;
+      wsp<int32_t>(c, c.rank, c.lay.tok_pass)[slot] = pass;
+      wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- enqueue
+
+__global__ void __launch_bounds__(kTokThreads) enqueue_kernel(DevCtx c, int layer, const int32_t* __restrict__ slots,
+                                                              int n, const float* __restrict__ logits,
+                                                              const int32_t* __restrict__ tidx,
+                                                              const float* __restrict__ tw) {
+  __shared__ PendingLeg legs[kTPC * kMaxKS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int chunk = blockIdx.x; chunk * kTPC < n; chunk += gridDim.x) {
+    for (int t = 0; t < kTPW; ++t) {
+      const int lt = warp * kTPW + t;
+      const int i = chunk * kTPC + lt;
+      PendingLeg* my = legs + lt * c.KS;
+      if (lane < c.KS) my[lane].r = -1;
+      if (i >= n) continue;
+      const int slot = slots[i];
+      if (slot < 0 || slot >= c.T) { if (lane == 0) raise_fault(c, F_SLOT_RANGE, slot, c.T, 1); continue; }
+      int idx[kMaxKS];
+      float w[kMaxKS];
+      if (logits) {
+        route_warp(logits + (uint64_t)i * c.E, c.E, c.K, lane, idx, w);
+      } else {
+        for (int k = 0; k < c.K; ++k) { idx[k] = tidx[(uint64_t)i * c.K + k]; w[k] = tw[(uint64_t)i * c.K + k]; }
+      }
+      if (lane < c.K) {
+        wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = idx[lane];
+        wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = w[lane];
+      }
+      if (lane == 0) {
+        wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
+        wsp<int32_t>(c, c.rank, c.lay.tok_layer)[slot] = layer;
+      }
+      make_legs(c, layer, slot, idx, w, lane, my);
+    }
+    __syncthreads();
+    scatter_legs(c, legs, kTPC * c.KS);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------- combine ring drain
+// Single warp: n = published (commit) - head; commits are only ever observed after the entry
+// writes (release/acquire), and when commit != reserve (a producer mid-flight on a peer) the
+// published prefix is found by scanning the per-entry seq flags.
+__global__ void cdrain_kernel(DevCtx c) {
+  uint32_t* ctr = wsp<uint32_t>(c, c.rank, c.lay.cctr);
+  amoe_leg* ring = wsp<amoe_leg>(c, c.rank, c.lay.cring);
+  int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
+  const int lane = threadIdx.x;
+  uint32_t head = ctr[2];
+  uint32_t n;
+  uint32_t cm = ld_acquire(ctr + 1);
+  uint32_t rv = ld_relaxed(ctr + 0);
+  if (cm == rv) {
+    n = cm - head;
+  } else {
+    n = 0;
+    for (;;) {
+      const uint32_t pos = head + n + lane;
+      const bool ok = (pos - head) < (rv - head) && ld_acquire(&ring[pos & c.cring_mask].seq) == pos + 1u;
+      const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+      if (bad) { n += __ffs(bad) - 1; break; }
+      n += 32;
+    }
+  }
+  if (n > c.cring_cap) { if (lane == 0) raise_fault(c, F_CRING_OVERFLOW, rv, head, 0); n = 0; }
+  if (lane == 0) {
+    info[0] = (int32_t)n;
+    info[1] = (int32_t)head;
+    ctr[2] = head + n;
+  }
+}
+
+// ---------------------------------------------------------------------------- combine (a8)
+
+template <typename T>
+__global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int retire_pass) {
+  using V = Vec<T>;
+  __shared__ PendingLeg legs[kTPC * kMaxKS];
+  __shared__ unsigned long long s_merged, s_retired;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
+  const int n = info[0];
+  const uint32_t start = (uint32_t)info[1];
+  const amoe_leg* ring = wsp<amoe_leg>(c, c.rank, c.lay.cring);
+  T* hbase = wsp<T>(c, c.rank, c.lay.h);
+  T* xbase = wsp<T>(c, c.rank, c.lay.x);
+  const T* pool = wsp<T>(c, c.rank, c.lay.pool);
+  const float* tokw = wsp<float>(c, c.rank, c.lay.tok_w);
+  int32_t* tlayer = wsp<int32_t>(c, c.rank, c.lay.tok_layer);
+  int32_t* tpass = wsp<int32_t>(c, c.rank, c.lay.tok_pass);
+  if (threadIdx.x == 0) { s_merged = 0; s_retired = 0; }
+  __syncthreads();
+  for (int chunk = blockIdx.x; chunk * kTPC < n; chunk += gridDim.x) {
+    for (int t = 0; t < kTPW; ++t) {
+      const int lt = warp * kTPW + t;
+      const int i = chunk * kTPC + lt;
+      PendingLeg* my = legs + lt * c.KS;
+      if (lane < c.KS) my[lane].r = -1;
+      if (i >= n) continue;
+      const uint32_t pos = start + (uint32_t)i;
+      const amoe_leg e = ring[pos & c.cring_mask];
+      if (e.seq != pos + 1u) { if (lane == 0) raise_fault(c, F_STALE_ENTRY, 0xffffffffu, pos, e.seq); continue; }
+      const int slot = e.token_slot;
+      float w[kMaxKS];
+      for (int k = 0; k < c.K; ++k) w[k] = tokw[(uint64_t)slot * c.K + k];
+      T* h = hbase + (uint64_t)slot * c.d;
+      const T* legrow = pool + (uint64_t)slot * c.KS * c.d;
+      // h_new = store(h + Σ_k w_k O_k + Σ_j O_shared_j), ascending k then j, no FMA (c9)
+      float ss = 0.f;
+      for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
+        float acc[V::N], o[V::N];
+        V::load(h + col, acc);
+        for (int k = 0; k < c.K; ++k) {
+          V::load(legrow + (uint64_t)k * c.d + col, o);
+#pragma unroll
+          for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(w[k], o[j]));
+        }
+        for (int k = c.K; k < c.KS; ++k) {
+          V::load(legrow + (uint64_t)k * c.d + col, o);
+#pragma unroll
+          for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], o[j]);
+        }
+        V::store(h + col, acc);
+#pragma unroll
+        for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[j]); ss += r * r; }
+      }
+      ss = warp_sum(ss);
+      rmsnorm_row<T>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);
+      int layer = tlayer[slot] + 1;
+      int pass = tpass[slot];
+      if (layer == c.L) { layer = 0; ++pass; }
+      if (lane == 0) { tlayer[slot] = layer; tpass[slot] = pass; atomicAdd(&s_merged, 1ull); }
+      if (pass >= retire_pass) {
+        if (lane == 0) atomicAdd(&s_retired, 1ull);
+        continue;
+      }
+      if (!c.router) { if (lane == 0) raise_fault(c, F_NO_ROUTER, slot, layer, pass); continue; }
+      int idx[kMaxKS];
+      float wn[kMaxKS];
+      const float* z = c.router + (((uint64_t)(pass % c.n_tab) * c.L + layer) * c.T + slot) * c.E;
+      route_warp(z, c.E, c.K, lane, idx, wn);
+      if (lane < c.K) {
+        wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = idx[lane];
+        wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = wn[lane];
+      }
+      if (lane == 0) wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
+      make_legs(c, layer, slot, idx, wn, lane, my);
+    }
+    __syncthreads();
+    scatter_legs(c, legs, kTPC * c.KS);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long* st = wsp<unsigned long long>(c, c.rank, c.lay.stats);
+    if (s_merged) atomicAdd(st + 0, s_merged);
+    if (s_retired) atomicAdd(st + 1, s_retired);
+  }
+}
+
+__global__ void announce_kernel(DevCtx c, uint32_t epoch) {
+  const int r = threadIdx.x;
+  if (r < c.G) st_release(wsp<uint32_t>(c, r, c.lay.done) + c.rank, epoch, r != c.rank);
+}
+
+// ---------------------------------------------------------------------------- launchers
+
+int launch_token_init(const DevCtx& c, const int32_t* slots, int n, const void* h0, int pass, cudaStream_t s) {
+  const int grid = (n + kTokWarps - 1) / kTokWarps < 1184 ? (n + kTokWarps - 1) / kTokWarps : 1184;
+  if (n <= 0) return 0;
+  if (c.dtype == AMOE_BF16)
+    token_init_kernel<__nv_bfloat16><<<grid, kTokThreads, 0, s>>>(c, slots, n, (const __nv_bfloat16*)h0, pass);
+  else
+    token_init_kernel<float><<<grid, kTokThreads, 0, s>>>(c, slots, n, (const float*)h0, pass);
+  return 1;
+}
+
+int launch_enqueue(const DevCtx& c, int layer, const int32_t* slots, int n, const float* logits,
+                   const int32_t* tidx, const float* tw, cudaStream_t s) {
+  if (n <= 0) return 0;
+  int grid = (n + kTPC - 1) / kTPC;
+  if (grid > 1184) grid = 1184;
+  enqueue_kernel<<<grid, kTokThreads, 0, s>>>(c, layer, slots, n, logits, tidx, tw);
+  return 1;
+}
+
+int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
+  cdrain_kernel<<<1, 32, 0, s>>>(c);
+  // grid sized for the worst case (all homed tokens ready); idle CTAs exit at once
+  int grid = (c.T + kTPC - 1) / kTPC;
+  if (grid > 1184) grid = 1184;
+  if (c.dtype == AMOE_BF16) combine_kernel<__nv_bfloat16><<<grid, kTokThreads, 0, s>>>(c, retire_pass);
+  else combine_kernel<float><<<grid, kTokThreads, 0, s>>>(c, retire_pass);
+  return 2;
+}
+
+int launch_announce(const DevCtx& c, uint32_t epoch, cudaStream_t s) {
+  announce_kernel<<<1, 32, 0, s>>>(c, epoch);
+  return 1;
+}
+
+}  // namespace amoe

@@ -1,0 +1,63 @@
+"""libamoe host-side checks that need no GPU: the library loads, exports every symbol the header
+declares, sizes workspaces, and its host scheduler equals the oracle's Algorithm 1/MTFS/FLFS."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import scheduler as osch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2505_08944_b200 import amoe, build
+    build.build()
+    amoe.load()
+    return amoe
+
+
+def test_library_exports_every_header_symbol(A):
+    hdr = open(os.path.join(ROOT, "include", "amoe.h")).read()
+    names = set(re.findall(r"^\s*(?:[a-z_0-9]+\s*\*?\s+)+\*?(amoe_[a-z_]+)\s*\(", hdr, re.M))
+    assert len(names) >= 25
+    lib = A.load()
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing
+    assert set(A.EXPORTS) == names          # the binding marshals exactly the ABI
+
+
+def test_status_strings(A):
+    lib = A.load()
+    for s in range(8):
+        assert lib.amoe_status_string(s)
+
+
+def test_workspace_sizing(A):
+    assert A.workspace_bytes(A.make_config(2, 8, 2, 0, 100, 256, 512)) == 0      # d % 64
+    assert A.workspace_bytes(A.make_config(2, 8, 9, 0, 128, 256, 512)) == 0      # K > 8
+    assert A.workspace_bytes(A.make_config(2, 4, 5, 0, 128, 256, 512)) == 0      # K > E
+    small = A.workspace_bytes(A.make_config(2, 8, 2, 0, 128, 256, 512))
+    big = A.workspace_bytes(A.make_config(2, 8, 2, 0, 128, 256, 1024))
+    assert 0 < small < big
+    mix = A.workspace_bytes(A.make_config(32, 8, 2, 0, 4096, 14336, 16384))
+    # h, x, pool, rings and the group scratch (tile, act, out) dominate: ~2.1 GB
+    assert 1.5e9 < mix < 3e9
+    g8 = A.workspace_bytes(A.make_config(32, 8, 2, 0, 4096, 14336, 16384, G=8, rank=3))
+    assert g8 > 0
+
+
+@pytest.mark.parametrize("policy", ["defrag", "mtfs", "flfs"])
+def test_host_scheduler_equals_oracle(A, policy):
+    g = np.random.default_rng(7)
+    for _ in range(3000):
+        NB, NQ, W = int(g.integers(1, 33)), int(g.integers(1, 10)), int(g.integers(0, 6))
+        delta = float(g.choice([0.5, 0.9, 0.25, 0.7]))
+        Q = (g.integers(0, 50, (NB, NQ)) * (g.random((NB, NQ)) < 0.3)).astype(np.uint32)
+        got = A.schedule(Q, NQ, policy, W, delta)
+        Ql = Q.tolist()
+        d32 = float(np.float32(delta))            # the C ABI takes δ as fp32
+        ref = osch.defrag(Ql, W, d32) if policy == "defrag" else osch.POLICIES[policy](Ql)
+        assert got == ref, (Ql, W, delta)
