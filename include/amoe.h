@@ -214,10 +214,20 @@ amoe_status amoe_run(amoe_ctx_t ctx, const amoe_run_params* params, int retire_p
                      amoe_run_stats* stats, void* stream);
 
 /* One decode pass end-to-end from HOST buffers: h0_host [T_slots, d] storage dtype (all slots)
- * is copied in, every token runs layers 0..L-1 once (amoe_token_init + amoe_enqueue(layer 0,
- * router table) + amoe_run), and the final h is copied to h_out_host. Synchronises `stream`. */
-amoe_status amoe_pass_host(amoe_ctx_t ctx, const void* h0_host, void* h_out_host, int pass,
-                           const amoe_run_params* params, amoe_run_stats* stats, void* stream);
+ * is copied in, and router_host [L][T_slots][E] fp32 (or NULL to keep the resident table) is
+ * copied into router table (pass mod n_tables); every token runs layers 0..L-1 once
+ * (amoe_token_init + amoe_enqueue(layer 0) + amoe_run) and the final h is copied to
+ * h_out_host [T_slots, d]. Synchronises `stream`. Multi-GPU: every rank calls it. */
+amoe_status amoe_pass_host(amoe_ctx_t ctx, const void* h0_host, const float* router_host, void* h_out_host,
+                           int pass, const amoe_run_params* params, amoe_run_stats* stats, void* stream);
+
+/* Per-stage device timing: when enabled, CUDA events bracket every launch of each stage on its
+ * stream (no synchronisation added). enable resets the accumulators (synchronises the device).
+ * read synchronises on the recorded events and returns summed milliseconds and the number of
+ * timed launches per stage: [0] rebatch (drain+gather), [1] FFN gate/up+SwiGLU, [2] FFN down,
+ * [3] forward, [4] combine (+route/scatter), [5] token_init/enqueue, [6..7] reserved. */
+amoe_status amoe_profile_enable(amoe_ctx_t ctx, int enable);
+amoe_status amoe_profile_read(amoe_ctx_t ctx, double ms_out[8], int64_t counts_out[8]);
 
 /* ---- introspection -------------------------------------------------------------------- */
 

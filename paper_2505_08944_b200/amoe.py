@@ -74,8 +74,10 @@ EXPORTS = {
     "amoe_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
     "amoe_combine": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "amoe_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, C.POINTER(RunStats), C.c_void_p]),
-    "amoe_pass_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(RunParams),
+    "amoe_pass_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(RunParams),
                                  C.POINTER(RunStats), C.c_void_p]),
+    "amoe_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "amoe_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "amoe_get_buffer": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     "amoe_hosted": (C.c_int, [C.c_void_p]),
     "amoe_ring_cap": (C.c_int, [C.c_void_p]),
@@ -299,13 +301,23 @@ class Context:
         self._chk(self.lib.amoe_run(self.h, C.byref(p), retire_pass, C.byref(st), _stream(stream)), "amoe_run")
         return st.as_dict()
 
-    def pass_host(self, h0_host: torch.Tensor, h_out_host: torch.Tensor, pass_idx=0, policy="defrag", W=4,
-                  delta=0.5, grouped=True, stream=None):
+    def pass_host(self, h0_host: torch.Tensor, h_out_host: torch.Tensor, router_host: torch.Tensor | None = None,
+                  pass_idx=0, policy="defrag", W=4, delta=0.5, grouped=True, stream=None):
         p = RunParams(POLICIES[policy], W, delta, 1 if grouped else 0, 0)
         st = RunStats()
-        self._chk(self.lib.amoe_pass_host(self.h, _p(h0_host), _p(h_out_host), pass_idx, C.byref(p), C.byref(st),
-                                          _stream(stream)), "amoe_pass_host")
+        self._chk(self.lib.amoe_pass_host(self.h, _p(h0_host), _p(router_host), _p(h_out_host), pass_idx,
+                                          C.byref(p), C.byref(st), _stream(stream)), "amoe_pass_host")
         return st.as_dict()
+
+    STAGES = ("rebatch", "ffn_gateup", "ffn_down", "forward", "combine", "admit")
+
+    def profile_enable(self, on=True):
+        self._chk(self.lib.amoe_profile_enable(self.h, 1 if on else 0), "amoe_profile_enable")
+
+    def profile_read(self):
+        ms, n = (C.c_double * 8)(), (C.c_int64 * 8)()
+        self._chk(self.lib.amoe_profile_read(self.h, ms, n), "amoe_profile_read")
+        return {s: (float(ms[i]), int(n[i])) for i, s in enumerate(self.STAGES)}
 
     # -- introspection
     def buffer(self, name, dtype=None, shape=None):

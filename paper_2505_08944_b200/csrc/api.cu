@@ -21,7 +21,7 @@ int launch_announce(const DevCtx&, uint32_t, cudaStream_t);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
-int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, int, cudaStream_t);
+int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, int, cudaStream_t, int);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
 int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
 }  // namespace amoe
@@ -57,6 +57,32 @@ struct amoe_ctx {
   cudaStream_t last_stream;
   std::vector<MapCacheEntry> map_cache;
   int32_t* scratch_qinfo;
+  // per-stage device timing (amoe_profile_*): CUDA events bracket each stage on its stream
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  double prof_ms[8] = {0};
+  int64_t prof_n[8] = {0};
+};
+
+enum Stage { ST_REBATCH = 0, ST_GATEUP = 1, ST_DOWN = 2, ST_FORWARD = 3, ST_COMBINE = 4, ST_ENQUEUE = 5 };
+
+static cudaEvent_t ev_get(amoe_ctx* c) {
+  if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct StageTimer {
+  amoe_ctx* c; int stage; cudaStream_t s; cudaEvent_t a = nullptr;
+  StageTimer(amoe_ctx* c_, int st, cudaStream_t s_) : c(c_), stage(st), s(s_) {
+    if (c->prof) { a = ev_get(c); cudaEventRecord(a, s); }
+  }
+  ~StageTimer() {
+    if (c->prof) { cudaEvent_t b = ev_get(c); cudaEventRecord(b, s); c->recs.push_back({stage, a, b}); }
+  }
 };
 
 static PFN_encodeTiled get_encoder() {
@@ -313,6 +339,7 @@ amoe_status amoe_set_router(amoe_ctx_t c, const float* table, int n_tables) {
 amoe_status amoe_token_init(amoe_ctx_t c, const int32_t* slots, int T, const void* h0, int pass, void* stream) {
   if (!c || T < 0 || (T > 0 && (!slots || !h0))) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  StageTimer tm(c, ST_ENQUEUE, s);
   c->launches += launch_token_init(c->dc, slots, T, h0, pass, s);
   c->admitted += T;
   c->last_stream = s;
@@ -327,6 +354,7 @@ amoe_status amoe_enqueue(amoe_ctx_t c, int layer, const int32_t* slots, int T, c
   cudaStream_t s = (cudaStream_t)stream;
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
+  StageTimer tm(c, ST_ENQUEUE, s);
   c->launches += launch_enqueue(c->dc, layer, slots, T, logits, topk_idx, topk_w, s);
   c->last_stream = s;
   CK(cudaGetLastError());
@@ -397,6 +425,7 @@ amoe_status amoe_rebatch(amoe_ctx_t c, const amoe_group* g, int max_tokens, void
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
   cudaStream_t s = (cudaStream_t)stream;
+  StageTimer tm(c, ST_REBATCH, s);
   c->launches += launch_drain(c->dc, gd, s);
   c->launches += launch_gather(c->dc, gd, c->num_sms, s);
   c->last_stream = s;
@@ -423,8 +452,16 @@ amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
     f.qinfo = g->qinfo;
     f.wmaps = reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps);
     for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
-    c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, c->num_sms, s);
+    {
+      StageTimer tm(c, ST_GATEUP, s);
+      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, c->num_sms, s, 1);
+    }
+    {
+      StageTimer tm(c, ST_DOWN, s);
+      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, c->num_sms, s, 2);
+    }
   } else {
+    StageTimer tm(c, ST_GATEUP, s);
     c->launches += launch_ffn_simt(c->dc, g->nq, g->qinfo, wslot, reinterpret_cast<const uint64_t*>(c->ws + c->lay.wptrs),
                                    g->tile, g->act, g->out, c->num_sms, s);
   }
@@ -440,6 +477,7 @@ amoe_status amoe_forward(amoe_ctx_t c, const amoe_group* g, void* stream) {
   if (st != AMOE_OK) return st;
   if (!g->out) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  StageTimer tm(c, ST_FORWARD, s);
   c->launches += launch_forward(c->dc, gd, c->num_sms, s);
   c->last_stream = s;
   CK(cudaGetLastError());
@@ -451,6 +489,7 @@ amoe_status amoe_combine(amoe_ctx_t c, int retire_pass, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   DevCtx dc = c->dc;
   if (!dc.router) { dc.n_tab = 1; }
+  StageTimer tm(c, ST_COMBINE, s);
   c->launches += launch_combine(dc, retire_pass, s);
   c->last_stream = s;
   CK(cudaGetLastError());
@@ -623,8 +662,8 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   return AMOE_OK;
 }
 
-amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, void* h_out_host, int pass, const amoe_run_params* p,
-                           amoe_run_stats* stats, void* stream) {
+amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, const float* router_host, void* h_out_host, int pass,
+                           const amoe_run_params* p, amoe_run_stats* stats, void* stream) {
   if (!c || !h0_host || !h_out_host || !p || !c->dc.router) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = (size_t)c->cfg.T_slots * c->cfg.d * c->dc.esize;
@@ -636,6 +675,11 @@ amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, void* h_out_host, 
   for (int i = 0; i < c->cfg.T_slots; ++i) iota[i] = i;
   CK(cudaMemcpyAsync(slots, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->ws + c->lay.h, h0_host, bytes, cudaMemcpyHostToDevice, s));
+  if (router_host) {
+    const size_t tb = (size_t)c->cfg.L * c->cfg.T_slots * c->cfg.E * sizeof(float);
+    float* dst = const_cast<float*>(c->dc.router) + (size_t)(pass % c->dc.n_tab) * c->cfg.L * c->cfg.T_slots * c->cfg.E;
+    CK(cudaMemcpyAsync(dst, router_host, tb, cudaMemcpyHostToDevice, s));
+  }
   amoe_status st = amoe_token_init(c, slots, c->cfg.T_slots, c->ws + c->lay.h, pass, s);
   if (st != AMOE_OK) return st;
   const float* z0 = c->dc.router + (uint64_t)(pass % c->dc.n_tab) * c->cfg.L * c->cfg.T_slots * c->cfg.E;
@@ -647,8 +691,36 @@ amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, void* h_out_host, 
   return AMOE_OK;
 }
 
+amoe_status amoe_profile_enable(amoe_ctx_t c, int enable) {
+  if (!c) return AMOE_EINVAL;
+  CK(cudaDeviceSynchronize());
+  for (auto& r : c->recs) { c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b); }
+  c->recs.clear();
+  for (int i = 0; i < 8; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+  c->prof = enable != 0;
+  return AMOE_OK;
+}
+
+amoe_status amoe_profile_read(amoe_ctx_t c, double* ms_out, int64_t* counts_out) {
+  if (!c || !ms_out || !counts_out) return AMOE_EINVAL;
+  for (auto& r : c->recs) {
+    CK(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    c->prof_ms[r.stage] += ms;
+    c->prof_n[r.stage] += 1;
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->recs.clear();
+  for (int i = 0; i < 8; ++i) { ms_out[i] = c->prof_ms[i]; counts_out[i] = c->prof_n[i]; }
+  return AMOE_OK;
+}
+
 amoe_status amoe_destroy(amoe_ctx_t c) {
   if (!c) return AMOE_EINVAL;
+  for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
   delete c;
   return AMOE_OK;

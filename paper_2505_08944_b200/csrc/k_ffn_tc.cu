@@ -293,8 +293,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
 // ------------------------------------------------------------------ launchers
 
 
+// part 1: gate/up + SwiGLU -> act; part 2: down -> out.
 int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_tile, const CUtensorMap& tm_act,
-                  void* act, void* out, int num_sms, cudaStream_t s) {
+                  void* act, void* out, int num_sms, cudaStream_t s, int part) {
   using namespace tc;
   static bool attr_done = false;
   if (!attr_done) {
@@ -315,7 +316,10 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.out_cols = c.ff;
   a.w_which = 0;
   a.out = reinterpret_cast<__nv_bfloat16*>(act);
-  ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a);
+  if (part == 1) {
+    ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a);
+    return 1;
+  }
   // down: N tiles of BN model columns
   const int bn = (c.d % 256 == 0) ? 256 : 128;
   a.n_tiles = c.d / bn;
@@ -326,7 +330,7 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   if (bn == 256) ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a);
   else ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a);
-  return 2;
+  return 1;
 }
 
 }  // namespace amoe

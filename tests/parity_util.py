@@ -21,11 +21,14 @@ def floored_err(got: np.ndarray, ref: np.ndarray) -> float:
 
 
 def row_l2_err(got: np.ndarray, ref: np.ndarray) -> float:
+    """Mean over rows of ‖got - ref‖₂ / ‖ref‖₂ (diagnostic; a systematic bug — a wrong operand,
+    truncation instead of RNE, a missing rounding — raises every row, rounding-order noise does
+    not. The max over rows is shape-dependent noise at small widths, hence the mean)."""
     got = np.asarray(got, np.float64).reshape(-1, ref.shape[-1])
     ref = np.asarray(ref, np.float64).reshape(-1, ref.shape[-1])
     if not ref.size:
         return 0.0
-    return float(np.max(np.linalg.norm(got - ref, axis=1) / (np.linalg.norm(ref, axis=1) + 1e-30)))
+    return float(np.mean(np.linalg.norm(got - ref, axis=1) / (np.linalg.norm(ref, axis=1) + 1e-30)))
 
 
 def ulp_err(got: np.ndarray, ref: np.ndarray, dtype: str) -> float:
