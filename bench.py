@@ -133,7 +133,7 @@ def cpu_oracle_sample(spec, seed, budget_s=15.0, max_tokens=4096):
 
 def run_reference(args):
     ws, rank, _ = dist_env()
-    if rank != 0:
+    if rank != 0:   # rank 0 alone runs the CPU oracle; the other ranks exit without work
         return
     import workload as wl
     spec = wl.CONFIGS[args.config]
@@ -171,8 +171,9 @@ def main():
 
     import workload as wl
     from paper_2505_08944_b200 import amoe
+    from paper_2505_08944_b200 import dist as D
 
-    G, rank, local = dist_env()
+    G, rank, local = D.env()
     assert G == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {G}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -185,15 +186,7 @@ def main():
     cfg = amoe.make_config(L, E, K, S, d, ff, T, G=G, rank=rank, dtype="bf16")
     nbytes = amoe.workspace_bytes(cfg)
     if G > 1:
-        import torch.distributed._symmetric_memory as symm_mem
-        try:
-            symm_mem.set_backend("CUDA")
-        except Exception:
-            pass
-        ws = symm_mem.empty(nbytes + 256, dtype=torch.uint8, device=dev)
-        hdl = symm_mem.rendezvous(ws, dist.group.WORLD)
-        ptrs = [int(p) for p in hdl.buffer_ptrs]
-        assert all(p % 256 == 0 for p in ptrs), "symmetric buffers must be 256-B aligned"
+        ws, ptrs = D.peer_workspace(nbytes + 256, dev)
         ctx = amoe.Context(cfg, workspace=ws, device=dev)
         ctx.import_peers(ptrs)
     else:
@@ -204,9 +197,7 @@ def main():
     gen.manual_seed(args.seed * 1000 + rank)
     wts = []
     for l in range(L):
-        for e in list(range(E)) + [E + j for j in range(S)]:
-            if e < E and e % G != rank:
-                continue
+        for e in D.hosted_experts(E, S, G, rank):
             w1 = torch.empty(ff, d, dtype=torch.bfloat16, device=dev).normal_(0, d ** -0.5, generator=gen)
             w3 = torch.empty(ff, d, dtype=torch.bfloat16, device=dev).normal_(0, d ** -0.5, generator=gen)
             w2 = torch.empty(d, ff, dtype=torch.bfloat16, device=dev).normal_(0, ff ** -0.5, generator=gen)
@@ -228,9 +219,7 @@ def main():
         ctx.enqueue(0, slots, logits=table[p % n_tab, 0])
         return ctx.run(retire_pass=p + 1, policy=policy, grouped=grouped)
 
-    def barrier():
-        if G > 1:
-            dist.barrier()
+    barrier = D.barrier
 
     for w in range(args.warmup):
         step(w)
@@ -261,12 +250,7 @@ def main():
     ctx.check()
     token_layers = sum(r["token_layers"] for r in runs)
     legs = sum(r["legs"] for r in runs)
-    if G > 1:
-        t = torch.tensor([ms, token_layers, legs], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        ms, token_layers, legs = float(tmax[0]), int(t[1]), int(t[2])
+    ms, (token_layers, legs) = D.reduce_timing(ms, [token_layers, legs], device=dev)
     assert token_layers == G * T * L * args.steps, (token_layers, G * T * L * args.steps)
     value = token_layers / (ms / 1e3)
 
@@ -333,11 +317,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ems = e0.elapsed_time(e1)
-        if G > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t[0])
+        ems, _ = D.reduce_timing(e0.elapsed_time(e1), [], device=dev)
         line["e2e"] = {"value": G * T * L * args.steps / (ems / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": int(h0_host.numel() * 2 + rt_host[0].numel() * 4),
                        "d2h_bytes_per_step": int(hout.numel() * 2),
