@@ -317,10 +317,9 @@ amoe_status amoe_set_expert(amoe_ctx_t c, int layer, int expert, const void* w1,
   CK(cudaMemcpy(c->ws + c->lay.wptrs + (uint64_t)slot * 24, ptrs, 24, cudaMemcpyHostToDevice));
   if (c->cfg.dtype == AMOE_BF16) {
     CUtensorMap maps[3];
-    const int bn = (c->cfg.d % 256 == 0) ? 256 : 128;
     if (!encode_bf16_2d(&maps[0], w1, c->cfg.ff, c->cfg.d, 128) ||
         !encode_bf16_2d(&maps[1], w3, c->cfg.ff, c->cfg.d, 128) ||
-        !encode_bf16_2d(&maps[2], w2, c->cfg.d, c->cfg.ff, bn))
+        !encode_bf16_2d(&maps[2], w2, c->cfg.d, c->cfg.ff, 128))
       return AMOE_ECUDA;
     CK(cudaMemcpy(c->ws + c->lay.wmaps + (uint64_t)slot * 3 * 128, maps, sizeof(maps), cudaMemcpyHostToDevice));
   }

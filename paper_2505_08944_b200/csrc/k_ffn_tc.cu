@@ -11,6 +11,8 @@
 // full/empty mbarriers; two 256-column fp32 accumulators in TMEM so the epilogue of tile i
 // overlaps the main loop of tile i+1. Tiles of a queue are rasterised in groups of 16 M-tiles
 // so concurrently running CTAs share the weight slab and the token rows through L2.
+#include <stdlib.h>
+
 #include "amoe_internal.cuh"
 
 namespace amoe {
@@ -199,7 +201,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
           tma_load_2d(sb, wb, kb * BK, nb * 128, full);
           tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
         } else {
-          tma_load_2d(sb, wb, kb * BK, nb * BN, full);
+          // weight maps have 128-row boxes: BN = 256 takes two loads
+#pragma unroll
+          for (int h = 0; h < BN / 128; ++h) tma_load_2d(sb + h * 128 * BK * 2, wb, kb * BK, nb * BN + h * 128, full);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
@@ -288,6 +292,234 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
   }
 }
 
+// ================================================================== CTA-pair variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile with UMMA M = 256.
+// CTA r loads A rows [m0 + 128 r, +128) and B rows [128 r, +128) of the 256-row B operand
+// (GATEUP: r = 0 -> W1 slab, r = 1 -> W3 slab; DOWN: W2 rows n0 + 128 r ...). The leader (r = 0)
+// issues the MMAs, which read A and B halves from both CTAs' shared memory; each CTA's TMEM
+// holds its own 128 rows x 256 fp32 columns, so the epilogue is per CTA as in the 1-CTA kernel.
+// Per CTA and per K=16 step this stages 8 KB instead of 12 KB (-33 % L2->SM bytes per FLOP).
+namespace tc2 {
+using namespace tc;
+constexpr int STAGES2 = 6;
+constexpr int HALF_BYTES = 128 * BK * 2;                     // 16 KB
+constexpr int STAGE2_BYTES = 2 * HALF_BYTES;                 // A half + B half = 32 KB
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 4096 + 1024;
+constexpr int BM2 = 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+// arrive on the barrier at this smem offset in both CTAs of the pair when the MMAs retire
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(bar_cluster) : "memory");
+}
+
+struct Sched2 {
+  int nq, n_tiles, total;
+  const int* n;
+  const int* pre;
+  __device__ __forceinline__ void decode(int t, int& q, int& m, int& nb) const {
+    int lo = 0, hi = nq - 1;
+    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (pre[mid] <= t) lo = mid; else hi = mid - 1; }
+    q = lo;
+    const int u = t - pre[q];
+    const int m_tiles = (n[q] + BM2 - 1) / BM2;
+    const int gsz = (GROUP_M / 2) * n_tiles;
+    const int g = u / gsz;
+    const int first_m = g * (GROUP_M / 2);
+    const int gm = min(m_tiles - first_m, GROUP_M / 2);
+    const int r = u - g * gsz;
+    m = first_m + r % gm;
+    nb = r / gm;
+  }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 1)
+ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* tiles = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  // bars: full[S], empty[S], tfull[2], tempty[2]   (full/tempty used in the leader only)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+  int* s_n = reinterpret_cast<int*>(tmem_holder + 4);
+  int* s_off = s_n + AMOE_MAX_GROUP;
+  int* s_pre = s_off + AMOE_MAX_GROUP;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int nq = args.nq;
+  for (int q = tid; q < nq; q += THREADS) { s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BM2 - 1) / BM2 * args.n_tiles; }
+    s_pre[nq] = acc;
+    for (int s = 0; s < STAGES2; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES2 + s]), 1); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
+      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 8);     // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch(&tmA);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_holder)), "r"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  Sched2 sc{nq, args.n_tiles, s_pre[nq], s_n, s_pre};
+  const int kb_n = args.k_blocks;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
+    // the leader's full barrier
+    int stage = 0; uint32_t phase = 0;
+    for (int t = cl; t < sc.total; t += ncl) {
+      int q, m, nb;
+      sc.decode(t, q, m, nb);
+      const int arow = s_off[q] + m * BM2 + (int)crank * 128;
+      const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
+      const CUtensorMap* bmap = (MODE == MODE_GATEUP) ? wb + crank : wb;
+      const int brow = (MODE == MODE_GATEUP) ? nb * 128 : nb * 256 + (int)crank * 128;
+      for (int kb = 0; kb < kb_n; ++kb) {
+        mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
+        const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
+        const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
+        if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
+        tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
+        tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
+        if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ===================== MMA issuer (leader CTA, single thread), UMMA 256 x 256 x 16
+    constexpr uint32_t idesc = idesc_bf16(BM2, 256);
+    int stage = 0; uint32_t phase = 0;
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = cl; t < sc.total; t += ncl) {
+      mbar_wait(smem_u32(&bars[2 * STAGES2 + 2 + acc]), acc_phase ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+      for (int kb = 0; kb < kb_n; ++kb) {
+        mbar_wait(smem_u32(&bars[stage]), phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
+        const uint64_t adesc = umma_desc_sw128(sa);
+        const uint64_t bdesc = umma_desc_sw128(sa + HALF_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+        umma_commit_pair(smem_u32(&bars[STAGES2 + stage]));       // frees the stage in both CTAs
+        if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
+      }
+      umma_commit_pair(smem_u32(&bars[2 * STAGES2 + acc]));        // accumulators ready in both
+      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (both CTAs): own 128 rows
+    const int ew = warp - 4;
+    int acc = 0; uint32_t acc_phase = 0;
+    const uint32_t tempty_leader0 = mapa(smem_u32(&bars[2 * STAGES2 + 2]), 0);
+    for (int t = cl; t < sc.total; t += ncl) {
+      int q, m, nb;
+      sc.decode(t, q, m, nb);
+      mbar_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase);
+      tc_fence_after();
+      const int row = m * BM2 + (int)crank * 128 + ew * 32 + lane;
+      const bool valid = row < s_n[q];
+      __nv_bfloat16* orow = args.out + (uint64_t)(s_off[q] + row) * args.out_ld;
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
+      if (MODE == MODE_GATEUP) {
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          float g[32], u[32];
+          tmem_ld32(taddr + ch * 32, g);
+          tmem_ld32(taddr + 128 + ch * 32, u);
+          if (valid) {
+            uint4 pk[4];
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              p2[j] = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
+            uint4* dst = reinterpret_cast<uint4*>(orow + nb * 128 + ch * 32);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < 8; ++ch) {
+          float v[32];
+          tmem_ld32(taddr + ch * 32, v);
+          const int col = nb * 256 + ch * 32;
+          if (valid && col < args.out_cols) {
+            uint4 pk[4];
+            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) p2[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+            uint4* dst = reinterpret_cast<uint4*>(orow + col);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(TMEM_COLS) : "memory");
+  }
+}
+}  // namespace tc2
+
 }  // namespace tc
 
 // ------------------------------------------------------------------ launchers
@@ -316,6 +548,39 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.out_cols = c.ff;
   a.w_which = 0;
   a.out = reinterpret_cast<__nv_bfloat16*>(act);
+  // CTA-pair kernels (default) need d % 256 == 0 and an even grid; AMOE_FFN_1CTA=1 forces 1-CTA
+  const char* ev = getenv("AMOE_FFN_1CTA");
+  const bool force1 = ev && ev[0] == '1';
+  const bool pair = !force1 && c.d % 256 == 0 && num_sms >= 2;
+  if (pair) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_GATEUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
+      cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
+      attr2 = true;
+    }
+    if (part == 2) {
+      a.n_tiles = c.d / 256;
+      a.k_blocks = c.ff / BK;
+      a.out_ld = c.d;
+      a.out_cols = c.d;
+      a.w_which = 2;
+      a.out = reinterpret_cast<__nv_bfloat16*>(out);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(num_sms & ~1));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = tc2::SMEM2_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (part == 1) cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a);
+    else cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a);
+    return 1;
+  }
   if (part == 1) {
     ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a);
     return 1;

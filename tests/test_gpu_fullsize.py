@@ -1,0 +1,99 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (grouped
+Algorithm-1 pick over all experts of a layer, CTA-pair tcgen05 kernels): one Mixtral-shaped layer
+(E=8, top-2, d=4096, ff=14336) with 16384 tokens in flight. The oracle recomputes sampled rows one
+by one (float64); integer results are checked in full."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as nx
+from parity_util import Problem, TOL, dev_tensor, floored_err, host_values, row_l2_err, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2505_08944_b200 import build
+    build.build()
+
+
+def _run_layer(P, ctx):
+    from paper_2505_08944_b200 import amoe
+    slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
+    ctx.token_init(slots, dev_tensor(P.h0[0], P.dtype), 0)
+    ctx.enqueue(0, slots, logits=torch.from_numpy(np.ascontiguousarray(P.tables[0][0, 0])).cuda())
+    gb = amoe.GroupBuffers(ctx, P.T * P.K + 128 * P.E)
+    gb.set_queues([(0, e) for e in range(P.E)])
+    ctx.rebatch(gb)
+    ctx.expert_ffn(gb)
+    torch.cuda.synchronize()
+    ctx.check()
+    return gb
+
+
+@pytest.mark.parametrize("d,ff,T", [(512, 1024, 2048), (2048, 1408, 4096)])
+def test_pair_kernel_matches_oracle_and_1cta(d, ff, T):
+    """CTA-pair (cta_group::2, M=256) kernels vs the oracle, and vs the 1-CTA kernels."""
+    P = Problem(L=1, E=8, K=2, S=0, d=d, ff=ff, T=T, seed=11)
+    ctx = P.make_ctx()
+    gb = _run_layer(P, ctx)
+    n, off, _ = gb.info()
+    tile, out = to_np(gb.tile), to_np(gb.out)
+    out_pair = out.copy()
+    for i in range(P.E):
+        rows = slice(off[i], off[i] + n[i])
+        ref = nx.expert_ffn(tile[rows], *P.W[(0, i)])
+        assert floored_err(out[rows], ref) <= TOL["bf16"]
+        assert row_l2_err(out[rows], ref) <= 2e-3
+    os.environ["AMOE_FFN_1CTA"] = "1"
+    try:
+        ctx2 = P.make_ctx()
+        gb2 = _run_layer(P, ctx2)
+    finally:
+        os.environ.pop("AMOE_FFN_1CTA")
+    out1 = to_np(gb2.out)
+    for i in range(P.E):
+        rows = slice(off[i], off[i] + n[i])
+        assert floored_err(out1[rows], out_pair[rows]) <= 2.0 ** -8
+
+
+@pytest.mark.slow
+def test_mixtral_layer_fullsize_sampled():
+    P = Problem(L=1, E=8, K=2, S=0, d=4096, ff=14336, T=16384, seed=12, n_tab=1)
+    ctx = P.make_ctx()
+    gb = _run_layer(P, ctx)
+    n, off, _ = gb.info()
+    idx, w = nx.route_topk(P.logits(0, 0), P.K)
+    hist = np.bincount(idx.ravel(), minlength=P.E)
+    assert np.array_equal(n, hist)                              # counts = router histogram
+    meta = gb.meta.cpu().numpy()
+    x = ctx.state()["x"]
+    g = np.random.default_rng(0)
+    for i in range(P.E):
+        # sampled rows: first, last and two random rows of every expert's segment
+        picks = sorted({0, n[i] - 1, *g.integers(0, n[i], 2).tolist()})
+        rows = off[i] + np.array(picks)
+        tile_rows = to_np(gb.tile[torch.from_numpy(rows).cuda()])
+        slots = meta[rows, 0]
+        assert np.array_equal(tile_rows, to_np(x[torch.from_numpy(slots).long().cuda()]))
+        ref = nx.expert_ffn(tile_rows, *P.W[(0, i)])
+        got = to_np(gb.out[torch.from_numpy(rows).cuda()])
+        assert floored_err(got, ref) <= TOL["bf16"], (i, floored_err(got, ref))
+        assert row_l2_err(got, ref) <= 2e-3
+    # forward + combine: bit-exact merge for every token
+    st = ctx.state()
+    h_before = to_np(st["h"])
+    w_gpu = st["tok_w"].cpu().numpy().copy()
+    ctx.forward(gb)
+    ctx.combine(retire_pass=1)
+    torch.cuda.synchronize()
+    ctx.check()
+    st = ctx.state()
+    ref_h = nx.combine(h_before, w_gpu, to_np(st["pool"]), None, "bf16")
+    assert np.array_equal(to_np(st["h"]), ref_h)
+    assert int(st["stats"][1]) == P.T                          # L = 1: every token retired
