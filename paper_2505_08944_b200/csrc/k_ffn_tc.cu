@@ -13,6 +13,8 @@
 // so concurrently running CTAs share the weight slab and the token rows through L2.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "amoe_internal.cuh"
 
 namespace amoe {
@@ -38,6 +40,7 @@ struct FfnArgs {
   int32_t out_ld;        // output row stride (elements)
   int32_t out_cols;      // valid output columns
   int32_t w_which;       // 0 (W1; W3 = +1) or 2 (W2) within a queue's 3 tensor maps
+  int32_t group_m;       // M tiles per raster group (L2 reuse of the weight slab)
   const int32_t* qinfo;
   const CUtensorMap* wmaps;
   __nv_bfloat16* out;
@@ -122,7 +125,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 // ------------------------------------------------------------------ tile schedule
 struct Sched {
-  int nq, n_tiles, total;
+  int nq, n_tiles, total, group;
   const int* n;
   const int* off;
   const int* pre;     // tile prefix per queue
@@ -132,10 +135,10 @@ struct Sched {
     q = lo;
     const int u = t - pre[q];
     const int m_tiles = (n[q] + BM - 1) / BM;
-    const int gsz = GROUP_M * n_tiles;
+    const int gsz = group * n_tiles;
     const int g = u / gsz;
-    const int first_m = g * GROUP_M;
-    const int gm = min(m_tiles - first_m, GROUP_M);
+    const int first_m = g * group;
+    const int gm = min(m_tiles - first_m, group);
     const int r = u - g * gsz;
     m = first_m + r % gm;
     nb = r / gm;
@@ -179,7 +182,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  Sched sc{nq, args.n_tiles, s_pre[nq], s_n, s_off, s_pre};
+  Sched sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_off, s_pre};
   const int kb_n = args.k_blocks;
 
   if (warp == 0 && lane == 0) {
@@ -348,7 +351,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
 }
 
 struct Sched2 {
-  int nq, n_tiles, total;
+  int nq, n_tiles, total, group;
   const int* n;
   const int* pre;
   __device__ __forceinline__ void decode(int t, int& q, int& m, int& nb) const {
@@ -357,10 +360,10 @@ struct Sched2 {
     q = lo;
     const int u = t - pre[q];
     const int m_tiles = (n[q] + BM2 - 1) / BM2;
-    const int gsz = (GROUP_M / 2) * n_tiles;
+    const int gsz = group * n_tiles;
     const int g = u / gsz;
-    const int first_m = g * (GROUP_M / 2);
-    const int gm = min(m_tiles - first_m, GROUP_M / 2);
+    const int first_m = g * group;
+    const int gm = min(m_tiles - first_m, group);
     const int r = u - g * gsz;
     m = first_m + r % gm;
     nb = r / gm;
@@ -407,7 +410,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  Sched2 sc{nq, args.n_tiles, s_pre[nq], s_n, s_pre};
+  Sched2 sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_pre};
   const int kb_n = args.k_blocks;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -552,6 +555,10 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const char* ev = getenv("AMOE_FFN_1CTA");
   const bool force1 = ev && ev[0] == '1';
   const bool pair = !force1 && c.d % 256 == 0 && num_sms >= 2;
+  // raster group: M tiles (of the kernel's M) sharing a weight slab through L2 (tuning knob)
+  const char* eg = getenv("AMOE_GROUP_M");
+  const int gm_rows = eg ? atoi(eg) : 2048;
+  a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
   if (pair) {
     static bool attr2 = false;
     if (!attr2) {

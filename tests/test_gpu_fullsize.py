@@ -59,7 +59,7 @@ def test_pair_kernel_matches_oracle_and_1cta(d, ff, T):
     out1 = to_np(gb2.out)
     for i in range(P.E):
         rows = slice(off[i], off[i] + n[i])
-        assert floored_err(out1[rows], out_pair[rows]) <= 2.0 ** -8
+        assert floored_err(out1[rows], out_pair[rows]) <= 2.0 ** -7
 
 
 @pytest.mark.slow

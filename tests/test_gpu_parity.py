@@ -133,9 +133,9 @@ def test_rebatch_and_expert_ffn(dtype):
         assert floored_err(out[rows], ref_out) <= TOL[dtype], (e, floored_err(out[rows], ref_out))
         assert row_l2_err(out[rows], ref_out) <= ROW_L2[dtype], (e, row_l2_err(out[rows], ref_out))
         # teacher-forced down projection: from the GPU's own activations only the fp32
-        # accumulation order differs -> about one storage rounding step (2^-8 for bf16)
+        # accumulation order differs -> at most one storage ulp (bf16: <= 2^-7 relative)
         ref_down = nx.to_storage((act[rows].astype(np.float64) @ w2.astype(np.float64).T).astype(np.float32), dtype)
-        assert floored_err(out[rows], ref_down) <= (2.0 ** -8 if dtype == "bf16" else TOL[dtype])
+        assert floored_err(out[rows], ref_down) <= (2.0 ** -7 if dtype == "bf16" else TOL[dtype])
     assert ctx.queue_depths().sum() == 0
 
 
