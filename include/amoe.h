@@ -76,7 +76,7 @@ typedef struct amoe_config {
   int32_t E;           /* routed experts per layer, <= AMOE_MAX_E */
   int32_t K;           /* top-K, 1 <= K <= 8, K <= E */
   int32_t S;           /* shared experts per layer (weight 1, run on the token's home), <= 4 */
-  int32_t d;           /* model width, multiple of 64 */
+  int32_t d;           /* model width, multiple of 128 */
   int32_t ff;          /* expert FFN width, multiple of 128 */
   int32_t G;           /* GPUs (ranks) in the box, 1..AMOE_MAX_G */
   int32_t rank;        /* this rank */
@@ -195,6 +195,12 @@ amoe_status amoe_rebatch(amoe_ctx_t ctx, const amoe_group* grp, int max_tokens, 
  * grp; act holds the bf16 SwiGLU activations. bf16: tcgen05/TMEM tensor-core kernels;
  * fp32: exact SIMT kernels. Rows beyond n[q] are not written. */
 amoe_status amoe_expert_ffn(amoe_ctx_t ctx, const amoe_group* grp, void* stream);
+
+/* a5 + a6 + a7 fused (what amoe_run uses): as amoe_expert_ffn, but the down-GEMM epilogue stores
+ * each output row directly into its token's home pool (NVLink peer store when remote) and
+ * counts it on the token's leg counter in 128-column pieces; grp->out is not written. The fp32
+ * mode runs amoe_expert_ffn then the amoe_forward kernel. */
+amoe_status amoe_expert_ffn_forward(amoe_ctx_t ctx, const amoe_group* grp, void* stream);
 
 /* a7 (return leg): store out rows into pool[home][token_slot][k] (NVLink store when remote),
  * bump the token's leg counter (release, system scope); the leg completing K (+S) appends the

@@ -162,6 +162,30 @@ __device__ __forceinline__ void write_leg(amoe_leg* ring, uint32_t mask, uint32_
   st_release(&e->seq, pos + 1u, sys);
 }
 
+// ------------------------------------------------------------------ token pool (a7 -> a8)
+// A leg's output row is returned in pieces of 128 columns (the fused down-GEMM epilogue stores
+// one N tile at a time); the token is complete when all (K+S) * d/128 pieces arrived.
+__device__ __forceinline__ uint32_t pieces_per_token(const DevCtx& c) { return (uint32_t)c.KS * (uint32_t)(c.d / 128); }
+
+// Count `pieces` returned pieces of token `slot` on `home` (release: the caller's pool stores
+// happen before); the arrival completing the token appends it to the home's combine ring.
+__device__ __forceinline__ void leg_pieces_done(const DevCtx& c, int home, int slot, int k, uint32_t pieces) {
+  const bool sys = c.G > 1;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(c.peer[home] + c.lay.legs_done) + slot;
+  const uint32_t old = atom_add_acqrel(cnt, pieces, sys);
+  const uint32_t total = pieces_per_token(c);
+  if (old + pieces > total) raise_fault(c, F_LEG_OVERCOUNT, slot, old + pieces, k);
+  if (old + pieces == total) {
+    uint32_t* cctr = reinterpret_cast<uint32_t*>(c.peer[home] + c.lay.cctr);
+    amoe_leg* cring = reinterpret_cast<amoe_leg*>(c.peer[home] + c.lay.cring);
+    const uint32_t pos = atom_add_relaxed(cctr, 1u, sys);
+    amoe_leg t;
+    t.token_slot = slot; t.k = 0; t.home = (int16_t)home; t.w = 0.f; t.seq = 0;
+    write_leg(cring, c.cring_mask, pos, t, sys);
+    red_add_release(cctr + 1, 1u, sys);
+  }
+}
+
 // ------------------------------------------------------------------ storage-type vectors
 // 16-byte vectors: 8 bf16 or 4 fp32 values.
 

@@ -21,7 +21,8 @@ int launch_announce(const DevCtx&, uint32_t, cudaStream_t);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
-int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, int, cudaStream_t, int);
+int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, const amoe_leg*,
+                  int, int, cudaStream_t, int);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
 int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
 }  // namespace amoe
@@ -133,7 +134,7 @@ static bool valid_cfg(const amoe_config* c) {
   if (!c) return false;
   if (c->L < 1 || c->E < 1 || c->E > AMOE_MAX_E || c->K < 1 || c->K > 8 || c->K > c->E) return false;
   if (c->S < 0 || c->S > 4 || c->K + c->S > kMaxKS) return false;
-  if (c->d < 64 || c->d % 64 || c->ff < 128 || c->ff % 128) return false;
+  if (c->d < 128 || c->d % 128 || c->ff < 128 || c->ff % 128) return false;
   if (c->G < 1 || c->G > AMOE_MAX_G || c->rank < 0 || c->rank >= c->G) return false;
   if (c->T_slots < 1 || c->dtype < 0 || c->dtype > 1 || c->max_batch < 0 || c->rows_cap < 0) return false;
   for (int e = 0; e < c->E; ++e)
@@ -432,8 +433,8 @@ amoe_status amoe_rebatch(amoe_ctx_t c, const amoe_group* g, int max_tokens, void
   return AMOE_OK;
 }
 
-amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
-  if (!c) return AMOE_EINVAL;
+// a5 + a6 (+ a7 when fuse: the down-GEMM epilogue stores rows straight into the home pools)
+static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaStream_t s) {
   GroupDev gd;
   int wslot[AMOE_MAX_GROUP];
   amoe_status st = make_group(c, g, 0, &gd, wslot);
@@ -441,7 +442,8 @@ amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
   if (!g->act || !g->out) return AMOE_EINVAL;
   for (int q = 0; q < g->nq; ++q)
     if (!c->hosted_flags[wslot[q] / 3]) return AMOE_EINVAL;   // weights not registered
-  cudaStream_t s = (cudaStream_t)stream;
+  for (int r = 0; r < c->cfg.G; ++r)
+    if (fuse && !c->dc.peer[r]) return AMOE_EPEER;
   if (c->cfg.dtype == AMOE_BF16) {
     const CUtensorMap* mt = cached_map(c, g->tile, g->rows_cap, c->cfg.d, 128);
     const CUtensorMap* ma = cached_map(c, g->act, g->rows_cap, c->cfg.ff, 128);
@@ -453,20 +455,37 @@ amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
     for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
     {
       StageTimer tm(c, ST_GATEUP, s);
-      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, c->num_sms, s, 1);
+      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, 0, c->num_sms, s, 1);
     }
     {
       StageTimer tm(c, ST_DOWN, s);
-      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, c->num_sms, s, 2);
+      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, fuse, c->num_sms, s, 2);
     }
   } else {
-    StageTimer tm(c, ST_GATEUP, s);
-    c->launches += launch_ffn_simt(c->dc, g->nq, g->qinfo, wslot, reinterpret_cast<const uint64_t*>(c->ws + c->lay.wptrs),
-                                   g->tile, g->act, g->out, c->num_sms, s);
+    {
+      StageTimer tm(c, ST_GATEUP, s);
+      c->launches += launch_ffn_simt(c->dc, g->nq, g->qinfo, wslot,
+                                     reinterpret_cast<const uint64_t*>(c->ws + c->lay.wptrs), g->tile, g->act, g->out,
+                                     c->num_sms, s);
+    }
+    if (fuse) {   // the exact fp32 mode keeps the separate forward kernel
+      StageTimer tm(c, ST_FORWARD, s);
+      c->launches += launch_forward(c->dc, gd, c->num_sms, s);
+    }
   }
   c->last_stream = s;
   CK(cudaGetLastError());
   return AMOE_OK;
+}
+
+amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  return expert_ffn(c, g, 0, (cudaStream_t)stream);
+}
+
+amoe_status amoe_expert_ffn_forward(amoe_ctx_t c, const amoe_group* g, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  return expert_ffn(c, g, 1, (cudaStream_t)stream);
 }
 
 amoe_status amoe_forward(amoe_ctx_t c, const amoe_group* g, void* stream) {
@@ -633,8 +652,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       }
       const int64_t l0 = c->launches;
       if ((st = amoe_rebatch(c, &g, 0, s)) != AMOE_OK) return st;
-      if ((st = amoe_expert_ffn(c, &g, s)) != AMOE_OK) return st;
-      if ((st = amoe_forward(c, &g, s)) != AMOE_OK) return st;
+      if ((st = amoe_expert_ffn_forward(c, &g, s)) != AMOE_OK) return st;
       if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
       rs.kernel_launches += c->launches - l0;
       rs.picks += 1;

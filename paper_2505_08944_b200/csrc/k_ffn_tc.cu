@@ -28,6 +28,8 @@ constexpr int B_BYTES = 256 * BK * 2;           // 32 KB (max BN = 256)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;
+// default FFN variant: 1-CTA (UMMA M=128); the CTA-pair variant is selected with AMOE_FFN_1CTA=0
+constexpr bool kDefault1Cta = true;
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;   // + barriers/tile tables + align
 
@@ -41,6 +43,8 @@ struct FfnArgs {
   int32_t out_cols;      // valid output columns
   int32_t w_which;       // 0 (W1; W3 = +1) or 2 (W2) within a queue's 3 tensor maps
   int32_t group_m;       // M tiles per raster group (L2 reuse of the weight slab)
+  int32_t fuse;          // DOWN: 1 = store rows straight into the home token pools (fused a7)
+  const amoe_leg* meta;  // [rows] drained legs (fused forward)
   const int32_t* qinfo;
   const CUtensorMap* wmaps;
   __nv_bfloat16* out;
@@ -147,9 +151,37 @@ struct Sched {
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
 
+// ------------------------------------------------------------------ fused a7 (forward)
+// DOWN epilogue destination of a row: the group's `out` buffer, or — fused forward — the leg's
+// slot in its home's token pool (local or NVLink peer store), pool[home][slot][k][:].
+template <int MODE>
+__device__ __forceinline__ __nv_bfloat16* down_row_dst(const FfnArgs& a, const DevCtx& dc, int grow, bool valid,
+                                                       amoe_leg& leg) {
+  if (MODE == MODE_DOWN && a.fuse) {
+    if (!valid) return nullptr;
+    leg = a.meta[grow];
+    return reinterpret_cast<__nv_bfloat16*>(dc.peer[leg.home] + dc.lay.pool) +
+           ((uint64_t)leg.token_slot * dc.KS + (uint64_t)leg.k) * dc.d;
+  }
+  return a.out + (uint64_t)grow * a.out_ld;
+}
+// After this thread stored its row's columns of N tile nb: count the 128-column pieces
+// (release: the stores happen before), completing arrivals append to the combine ring.
+__device__ __forceinline__ void down_row_done(const FfnArgs& a, const DevCtx& dc, const amoe_leg& leg, int nb, int bn,
+                                              unsigned long long* s_fwd) {
+  const int cols = min(bn, dc.d - nb * bn);
+  if (cols <= 0) return;
+  leg_pieces_done(dc, leg.home, leg.token_slot, leg.k, (uint32_t)(cols / 128));
+  if (nb == 0) {
+    atomicAdd(&s_fwd[0], 1ull);
+    if (leg.home != dc.rank) atomicAdd(&s_fwd[1], 1ull);
+  }
+}
+
 template <int MODE, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
-ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
+ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
+  __shared__ unsigned long long s_fwd[2];     // legs forwarded, of which remote
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -168,6 +200,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
     int acc = 0;
     for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BM - 1) / BM * args.n_tiles; }
     s_pre[nq] = acc;
+    s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES + s]), 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(smem_u32(&bars[2 * STAGES + a]), 1); mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -246,7 +279,8 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
       tc_fence_after();
       const int row = m * BM + ew * 32 + lane;
       const bool valid = row < s_n[q];
-      __nv_bfloat16* orow = args.out + (uint64_t)(s_off[q] + row) * args.out_ld;
+      amoe_leg leg;
+      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, s_off[q] + row, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
       if (MODE == MODE_GATEUP) {
 #pragma unroll 1
@@ -281,6 +315,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
             for (int j = 0; j < 4; ++j) dst[j] = pk[j];
           }
         }
+        if (args.fuse && valid) down_row_done(args, dc, leg, nb, BN, s_fwd);
       }
       tc_fence_before();
       mbar_arrive(smem_u32(&bars[2 * STAGES + 2 + acc]));
@@ -292,6 +327,11 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
   tc_fence_after();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(TMEM_COLS) : "memory");
+  }
+  if (MODE == MODE_DOWN && args.fuse && tid == 0) {
+    unsigned long long* st = wsp<unsigned long long>(dc, dc.rank, dc.lay.stats);
+    if (s_fwd[0]) atomicAdd(st + 2, s_fwd[0]);
+    if (s_fwd[1]) atomicAdd(st + 3, s_fwd[1]);
   }
 }
 
@@ -372,7 +412,8 @@ struct Sched2 {
 
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
-ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
+ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
+  __shared__ unsigned long long s_fwd[2];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -393,6 +434,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
     int acc = 0;
     for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BM2 - 1) / BM2 * args.n_tiles; }
     s_pre[nq] = acc;
+    s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES2; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES2 + s]), 1); }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
@@ -471,7 +513,8 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
       tc_fence_after();
       const int row = m * BM2 + (int)crank * 128 + ew * 32 + lane;
       const bool valid = row < s_n[q];
-      __nv_bfloat16* orow = args.out + (uint64_t)(s_off[q] + row) * args.out_ld;
+      amoe_leg leg;
+      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, s_off[q] + row, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
       if (MODE == MODE_GATEUP) {
 #pragma unroll 1
@@ -506,6 +549,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
             for (int j = 0; j < 4; ++j) dst[j] = pk[j];
           }
         }
+        if (args.fuse && valid) down_row_done(args, dc, leg, nb, 256, s_fwd);
       }
       tc_fence_before();
       __syncwarp();
@@ -517,6 +561,11 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
   __syncthreads();
   cluster_sync();
   tc_fence_after();
+  if (MODE == MODE_DOWN && args.fuse && tid == 0) {
+    unsigned long long* st = wsp<unsigned long long>(dc, dc.rank, dc.lay.stats);
+    if (s_fwd[0]) atomicAdd(st + 2, s_fwd[0]);
+    if (s_fwd[1]) atomicAdd(st + 3, s_fwd[1]);
+  }
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "r"(TMEM_COLS) : "memory");
   }
@@ -528,52 +577,51 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args) {
 // ------------------------------------------------------------------ launchers
 
 
-// part 1: gate/up + SwiGLU -> act; part 2: down -> out.
+// part 1: gate/up + SwiGLU -> act; part 2: down -> out, or (fuse) straight into the home pools.
 int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_tile, const CUtensorMap& tm_act,
-                  void* act, void* out, int num_sms, cudaStream_t s, int part) {
+                  void* act, void* out, const amoe_leg* meta, int fuse, int num_sms, cudaStream_t s, int part) {
   using namespace tc;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_GATEUP, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_DOWN, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_DOWN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_GATEUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
+    cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
     attr_done = true;
   }
   FfnArgs a{};
   a.nq = f.nq;
   a.qinfo = f.qinfo;
   a.wmaps = f.wmaps;
+  a.meta = meta;
   for (int q = 0; q < f.nq; ++q) a.wslot[q] = f.wslot[q];
-  // gate/up + SwiGLU: N tiles of 128 ff-columns (x2 for gate and up)
-  a.n_tiles = c.ff / 128;
-  a.k_blocks = c.d / BK;
-  a.out_ld = c.ff;
-  a.out_cols = c.ff;
-  a.w_which = 0;
-  a.out = reinterpret_cast<__nv_bfloat16*>(act);
-  // CTA-pair kernels (default) need d % 256 == 0 and an even grid; AMOE_FFN_1CTA=1 forces 1-CTA
+  // CTA-pair kernels need d % 256 == 0 and an even grid; AMOE_FFN_1CTA=1 forces 1-CTA, =0 pairs
   const char* ev = getenv("AMOE_FFN_1CTA");
-  const bool force1 = ev && ev[0] == '1';
+  const bool force1 = ev ? ev[0] == '1' : kDefault1Cta;
   const bool pair = !force1 && c.d % 256 == 0 && num_sms >= 2;
-  // raster group: M tiles (of the kernel's M) sharing a weight slab through L2 (tuning knob)
+  // raster group: rows of a queue sharing a weight slab through L2 (tuning knob)
   const char* eg = getenv("AMOE_GROUP_M");
   const int gm_rows = eg ? atoi(eg) : 2048;
   a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
+  const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
+  if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
+    a.n_tiles = c.ff / 128;
+    a.k_blocks = c.d / BK;
+    a.out_ld = c.ff;
+    a.out_cols = c.ff;
+    a.w_which = 0;
+    a.out = reinterpret_cast<__nv_bfloat16*>(act);
+  } else {                    // N tiles of bn model columns
+    a.n_tiles = c.d / bn;
+    a.k_blocks = c.ff / BK;
+    a.out_ld = c.d;
+    a.out_cols = c.d;
+    a.w_which = 2;
+    a.out = reinterpret_cast<__nv_bfloat16*>(out);
+    a.fuse = fuse;
+  }
   if (pair) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_GATEUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
-      cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
-      attr2 = true;
-    }
-    if (part == 2) {
-      a.n_tiles = c.d / 256;
-      a.k_blocks = c.ff / BK;
-      a.out_ld = c.d;
-      a.out_cols = c.d;
-      a.w_which = 2;
-      a.out = reinterpret_cast<__nv_bfloat16*>(out);
-    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(num_sms & ~1));
     cfg.blockDim = dim3(THREADS);
@@ -584,24 +632,13 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (part == 1) cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a);
-    else cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a);
+    if (part == 1) cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
+    else cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
     return 1;
   }
-  if (part == 1) {
-    ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a);
-    return 1;
-  }
-  // down: N tiles of BN model columns
-  const int bn = (c.d % 256 == 0) ? 256 : 128;
-  a.n_tiles = c.d / bn;
-  a.k_blocks = c.ff / BK;
-  a.out_ld = c.d;
-  a.out_cols = c.d;
-  a.w_which = 2;
-  a.out = reinterpret_cast<__nv_bfloat16*>(out);
-  if (bn == 256) ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a);
-  else ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a);
+  if (part == 1) ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a, c);
+  else if (bn == 256) ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
+  else ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
   return 1;
 }
 

@@ -143,29 +143,18 @@ __global__ void __launch_bounds__(kRowThreads) forward_kernel(DevCtx c, GroupDev
     const int row = off_s[q] + (r - pre[q]);
     const amoe_leg e = g.meta[row];
     const int home = e.home;
-    const bool sys = home != c.rank;
+    const bool sys = c.G > 1;            // all writers of a leg counter use one scope
     char* dst = reinterpret_cast<char*>(c.peer[home] + c.lay.pool) +
                 ((uint64_t)e.token_slot * c.KS + (uint64_t)e.k) * rowbytes;
     const char* src = reinterpret_cast<const char*>(g.out) + (uint64_t)row * rowbytes;
     warp_copy(dst, src, rowbytes, lane);
     __syncwarp();
     if (lane == 0) {
-      fence_sc(sys);
-      uint32_t* cnt = reinterpret_cast<uint32_t*>(c.peer[home] + c.lay.legs_done) + e.token_slot;
-      const uint32_t old = atom_add_acqrel(cnt, 1u, sys);
+      fence_sc(sys);       // the whole warp's row stores before the counter (cumulativity)
       atomicAdd(&s_legs, 1ull);
-      if (sys) atomicAdd(&s_remote, 1ull);
-      if (old + 1u > (uint32_t)c.KS) raise_fault(c, F_LEG_OVERCOUNT, e.token_slot, old + 1u, e.k);
-      if (old + 1u == (uint32_t)c.KS) {
-        // all legs present: append the token to its home's combine ring
-        uint32_t* cctr = reinterpret_cast<uint32_t*>(c.peer[home] + c.lay.cctr);
-        amoe_leg* cring = reinterpret_cast<amoe_leg*>(c.peer[home] + c.lay.cring);
-        const uint32_t pos = atom_add_relaxed(cctr, 1u, sys);
-        amoe_leg t = e;
-        t.k = 0;
-        write_leg(cring, c.cring_mask, pos, t, sys);
-        red_add_release(cctr + 1, 1u, sys);
-      }
+      if (home != c.rank) atomicAdd(&s_remote, 1ull);
+      // the whole row = d/128 pieces; the completing arrival appends to the combine ring
+      leg_pieces_done(c, home, e.token_slot, e.k, (uint32_t)(c.d / 128));
     }
   }
   __syncthreads();

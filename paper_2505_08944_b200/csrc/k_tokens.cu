@@ -71,12 +71,14 @@ __device__ void scatter_legs(const DevCtx& c, const PendingLeg* legs, int n) {
     const int key = active ? (r << 24 | q) : -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
-    const bool sys = r != c.rank;
+    // with peers, every producer of a ring (local or remote) uses system scope so that all
+    // release/acquire pairs on the shared counters are morally strong
+    const bool sys = c.G > 1;
     uint32_t pos0 = 0;
     if (active && lane == leader) {
       uint32_t* ctr = qctr_ptr(c, r, q);
       pos0 = atom_add_relaxed(ctr, (uint32_t)__popc(peers), sys);
-      if (!sys) {
+      if (r == c.rank) {
         uint32_t head = ld_relaxed(ctr + 2);
         if (pos0 + (uint32_t)__popc(peers) - head > c.ring_cap) raise_fault(c, F_RING_OVERFLOW, q, pos0, head);
       }

@@ -72,6 +72,35 @@ def main():
     res = []
     for v in args.variants.split(","):
         kind, rows = v.split(":")
+        if kind == "cublas":
+            # library reference on the same FLOPs: [legs x d] @ [d x 2ff] then [legs x ff] @ [ff x d]
+            X = torch.randn(legs, d, device="cuda", dtype=torch.bfloat16)
+            W13 = torch.randn(2 * ff, d, device="cuda", dtype=torch.bfloat16)
+            A = torch.randn(legs, ff, device="cuda", dtype=torch.bfloat16)
+            W2 = torch.randn(d, ff, device="cuda", dtype=torch.bfloat16)
+            for _ in range(3):
+                X @ W13.t(); A @ W2.t()
+            torch.cuda.synchronize()
+            p = sample_start()
+            t0, n = time.time(), 0
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            while time.time() - t0 < args.secs:
+                for _ in range(8):
+                    X @ W13.t(); A @ W2.t()
+                n += 8
+                torch.cuda.synchronize()
+            ev1.record()
+            torch.cuda.synchronize()
+            sm, pw = sample_stop(p)
+            ms = ev0.elapsed_time(ev1) / n
+            tf = flop / (ms / 1e3) / 1e12
+            r = {"variant": v, "legs": legs, "ms_per_ffn": round(ms, 3), "tflops": round(tf, 1), "sm_mhz": sm,
+                 "power_w": pw, "tflops_per_w": round(tf / pw, 3) if pw else None,
+                 "tflop_per_mhz": round(tf / sm, 3) if sm else None}
+            print(json.dumps(r), flush=True)
+            del X, W13, A, W2
+            continue
         os.environ["AMOE_FFN_1CTA"] = "1" if kind == "1cta" else "0"
         os.environ["AMOE_GROUP_M"] = rows
         for _ in range(3):
