@@ -12,6 +12,7 @@ constexpr int kTokThreads = 256;
 constexpr int kTokWarps = kTokThreads / kWarp;
 constexpr int kTPW = 4;                       // tokens per warp per chunk
 constexpr int kTPC = kTokWarps * kTPW;        // tokens per CTA chunk
+constexpr int kU = 4;                         // 16-byte chunks per lane batched in the merge
 
 struct PendingLeg {
   int32_t r;      // owner rank (-1 = inactive)
@@ -126,12 +127,22 @@ template <typename T>
 __device__ __forceinline__ void rmsnorm_row(const DevCtx& c, const T* h, T* x, float ss, int lane) {
   using V = Vec<T>;
   const float r = 1.0f / sqrtf(ss / (float)c.d + c.eps);
-  for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
-    float f[V::N];
-    V::load(h + col, f);
+  for (int col0 = lane * V::N; col0 < c.d; col0 += 4 * kWarp * V::N) {
+    float f[4][V::N];
 #pragma unroll
-    for (int j = 0; j < V::N; ++j) f[j] = f[j] * r;
-    V::store(x + col, f);
+    for (int u = 0; u < 4; ++u) {
+      const int col = col0 + u * kWarp * V::N;
+      if (col < c.d) V::load(h + col, f[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int col = col0 + u * kWarp * V::N;
+      if (col < c.d) {
+#pragma unroll
+        for (int j = 0; j < V::N; ++j) f[u][j] = f[u][j] * r;
+        V::store(x + col, f[u]);
+      }
+    }
   }
 }
 
@@ -276,24 +287,41 @@ __global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int reti
       for (int k = 0; k < c.K; ++k) w[k] = tokw[(uint64_t)slot * c.K + k];
       T* h = hbase + (uint64_t)slot * c.d;
       const T* legrow = pool + (uint64_t)slot * c.KS * c.d;
-      // h_new = store(h + Σ_k w_k O_k + Σ_j O_shared_j), ascending k then j, no FMA (c9)
+      // h_new = store(h + Σ_k w_k O_k + Σ_j O_shared_j), ascending k then j, no FMA (c9);
+      // shared legs use w = 1 (1·O == O exactly). kU 16-byte chunks per lane are loaded
+      // together per leg so each lane keeps kU loads in flight.
+      for (int k = c.K; k < c.KS; ++k) w[k] = 1.0f;
       float ss = 0.f;
-      for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
-        float acc[V::N], o[V::N];
-        V::load(h + col, acc);
-        for (int k = 0; k < c.K; ++k) {
-          V::load(legrow + (uint64_t)k * c.d + col, o);
+      for (int col0 = lane * V::N; col0 < c.d; col0 += kU * kWarp * V::N) {
+        float acc[kU][V::N];
 #pragma unroll
-          for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(w[k], o[j]));
+        for (int u = 0; u < kU; ++u) {
+          const int col = col0 + u * kWarp * V::N;
+          if (col < c.d) V::load(h + col, acc[u]);
         }
-        for (int k = c.K; k < c.KS; ++k) {
-          V::load(legrow + (uint64_t)k * c.d + col, o);
+        for (int k = 0; k < c.KS; ++k) {
+          float o[kU][V::N];
+          const T* src = legrow + (uint64_t)k * c.d;
 #pragma unroll
-          for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], o[j]);
+          for (int u = 0; u < kU; ++u) {
+            const int col = col0 + u * kWarp * V::N;
+            if (col < c.d) V::load(src + col, o[u]);
+          }
+          const float wk = w[k];
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int j = 0; j < V::N; ++j) acc[u][j] = __fadd_rn(acc[u][j], __fmul_rn(wk, o[u][j]));
         }
-        V::store(h + col, acc);
 #pragma unroll
-        for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[j]); ss += r * r; }
+        for (int u = 0; u < kU; ++u) {
+          const int col = col0 + u * kWarp * V::N;
+          if (col < c.d) {
+            V::store(h + col, acc[u]);
+#pragma unroll
+            for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[u][j]); ss += r * r; }
+          }
+        }
       }
       ss = warp_sum(ss);
       rmsnorm_row<T>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);

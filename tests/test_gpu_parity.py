@@ -287,6 +287,55 @@ def test_loopback_peers_match_single_gpu(G):
     assert remote > 0
 
 
+@pytest.mark.parametrize("G,d", [(2, 128), (4, 256)])
+def test_loopback_amoe_run_concurrent_ranks(G, d):
+    """The native multi-rank loop: G contexts on one GPU, each running amoe_run in its own host
+    thread on its own CUDA stream, concurrently. Legs cross ranks through peer rings (remote
+    reservations race with local producers), outputs return by one-sided stores, and each rank
+    keeps serving until every rank's done flag is set. Result: bit-identical to one rank."""
+    import threading
+    T = 128
+    P = Problem(L=2, E=8, K=2, S=0, d=d, ff=256, T=T, G=G, seed=14)
+    ctxs = [P.make_ctx(rank=r) for r in range(G)]
+    ptrs = [c.ws.data_ptr() for c in ctxs]
+    for c in ctxs:
+        c.import_peers(ptrs)
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    for r, c in enumerate(ctxs):
+        with torch.cuda.stream(streams[r]):
+            admit(c, P, rank=r)
+    torch.cuda.synchronize()
+    stats, errs = [None] * G, []
+
+    def worker(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                stats[r] = ctxs[r].run(retire_pass=2, stream=streams[r])
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append((r, e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "amoe_run did not terminate"
+    assert not errs, errs
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check()
+    assert sum(s["token_layers"] for s in stats) == G * T * P.L * 2
+    h = np.concatenate([to_np(c.state()["h"]) for c in ctxs])
+    P1 = Problem(L=2, E=8, K=2, S=0, d=d, ff=256, T=G * T, G=1, seed=14)
+    P1.tables = [np.concatenate(P.tables, axis=2)]
+    P1.h0 = [np.concatenate(P.h0)]
+    c1 = P1.make_ctx()
+    admit(c1, P1)
+    c1.run(retire_pass=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(h, to_np(c1.state()["h"]))
+
+
 # ---------------------------------------------------------------- device faults
 
 def test_fault_expert_out_of_range_is_latched():
