@@ -46,6 +46,15 @@ def parse():
     return ap.parse_args()
 
 
+def config_dict(spec, L, T, G, policy, grouped):
+    """The workload description shared by both arms' JSON lines."""
+    return {"workload": f"{spec.name}-shaped expert layers: L={L} E={spec.E} top-{spec.K} S={spec.S} d={spec.d} "
+                        f"ff={spec.ff}, {T} tokens in flight per GPU, Zipf s={spec.zipf_s} routing",
+            "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped,
+            "l2": "inputs larger than L2 (resident weights >> 126 MB); no flush",
+            "step": "one decode pass: every token through all L layers"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
@@ -96,25 +105,37 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------- CPU oracle
 
-def cpu_oracle_sample(spec, seed, budget_s=15.0, max_tokens=4096):
-    """Time the oracle (as it stands) on a bounded sample of the same workload: batches of
-    tokens through layer 0 of the configuration (routing, SwiGLU experts, combine, RMSNorm)."""
-    import numpy as np
+_ORACLE_INPUTS = {}
+
+
+def _oracle_inputs(spec, seed, max_tokens):
+    """Layer-0 weights, logits and hidden states of the workload (generated once, not timed)."""
     import workload as wl
-    from oracle import numerics as nx
-    try:
-        from threadpoolctl import threadpool_limits
-    except Exception:  # pragma: no cover
-        threadpool_limits = None
-    cores = len(os.sched_getaffinity(0))
-    ctxm = threadpool_limits(limits=cores) if threadpool_limits else None
-    try:
+    key = (spec.name, seed, max_tokens)
+    if key not in _ORACLE_INPUTS:
         W = [tuple(wl.f32_from_bf16_bits(a) for a in wl.expert_weights(seed, 0, e, spec.d, spec.ff))
              for e in range(spec.E)]
         SH = [tuple(wl.f32_from_bf16_bits(a) for a in wl.expert_weights(seed, 0, spec.E + j, spec.d, spec.ff))
               for j in range(spec.S)]
         z = wl.router_logits(seed, spec.L, min(spec.T, max_tokens), spec.E, layers=[0])[0]
         h = wl.f32_from_bf16_bits(wl.hidden0(seed, min(spec.T, max_tokens), spec.d))
+        _ORACLE_INPUTS.clear()
+        _ORACLE_INPUTS[key] = (W, SH, z, h)
+    return _ORACLE_INPUTS[key]
+
+
+def cpu_oracle_sample(spec, seed, budget_s=15.0, max_tokens=4096):
+    """Time the oracle (as it stands) on a bounded sample of the same workload: batches of
+    tokens through layer 0 of the configuration (routing, SwiGLU experts, combine, RMSNorm)."""
+    from oracle import numerics as nx
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    cores = len(os.sched_getaffinity(0))
+    W, SH, z, h = _oracle_inputs(spec, seed, max_tokens)
+    ctxm = threadpool_limits(limits=cores) if threadpool_limits else None
+    try:
         done, t0, batch = 0, time.perf_counter(), 64 if spec.d >= 2048 else 512
         while done < h.shape[0]:
             sl = slice(done, min(done + batch, h.shape[0]))
@@ -137,8 +158,10 @@ def run_reference(args):
         return
     import workload as wl
     spec = wl.CONFIGS[args.config]
+    # each step = one bounded sample (<= 128 tokens through layer 0, <= 10 s of oracle work);
+    # inputs are generated once before the warm-up (not timed)
     for _ in range(args.warmup):
-        cpu_oracle_sample(spec, args.seed, budget_s=5.0, max_tokens=64)
+        cpu_oracle_sample(spec, args.seed, budget_s=3.0, max_tokens=128)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -150,8 +173,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64-accum/bf16-storage",
             "data": "synthetic (seeded workload generator)",
-            "config": {"workload": spec.name, "L": spec.L, "E": spec.E, "K": spec.K, "S": spec.S, "d": spec.d,
-                       "ff": spec.ff, "T_slots": spec.T},
+            "config": config_dict(spec, spec.L, spec.T, args.gpus, args.policy, not args.ungrouped),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": "oracle",
                              "sample": r["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -281,11 +303,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
-        "config": {"workload": f"{spec.name}-shaped expert layers: L={L} E={E} top-{K} S={S} d={d} ff={ff}, "
-                               f"{T} tokens in flight per GPU",
-                   "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped,
-                   "l2": "inputs larger than L2 (resident weights >> 126 MB); no flush",
-                   "step": "one decode pass: every token through all L layers"},
+        "config": config_dict(spec, L, T, G, policy, grouped),
         "gpu_launches": int(launches),
         "clocks": clk,
         "roofline": {"bound": "tensor", "kernel": "ffn_tc_kernel<GATEUP> (tcgen05, fused SwiGLU)",
