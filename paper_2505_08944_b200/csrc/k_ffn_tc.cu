@@ -28,8 +28,10 @@ constexpr int B_BYTES = 256 * BK * 2;           // 32 KB (max BN = 256)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;
-// default FFN variant: 1-CTA (UMMA M=128); the CTA-pair variant is selected with AMOE_FFN_1CTA=0
-constexpr bool kDefault1Cta = true;
+// default FFN variant: the CTA pair (UMMA M=256, cta_group::2) when d % 256 == 0 — measured
+// 1.33 vs 1.27 TFLOP/s per W under the power cap (profiles/r01_ffn_power.md); AMOE_FFN_1CTA=1
+// selects the 1-CTA kernel (UMMA M=128), which also serves d % 256 != 0
+constexpr bool kDefault1Cta = false;
 constexpr uint32_t kSuspendNs = 0x10000;   // mbarrier try_wait suspend-time hint (ns)
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;   // + barriers/tile tables + align
@@ -157,7 +159,32 @@ struct Sched {
 // silu(g)·u = g·u / (1 + e^-g) with the SFU (ex2.approx, rcp.approx): ~6 instructions instead
 // of ~20 for expf + IEEE division. The result is rounded to bf16 (8 significant bits), so the
 // approximations (~2^-21 relative) change only rounding-boundary cases (parity: tests).
-__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g * u, 1.0f + __expf(-g)); }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// g very negative: 2^(+big) = inf, rcp(inf) = 0 -> 0; g very positive: rcp(1) -> g·u.
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  return (g * u) * rcp_approx(1.0f + ex2_approx(g * -1.4426950408889634f));
+}
+
+// The epilogue warps (threads [first, first+128)) wait for an accumulator: one elected thread
+// sleeps on the mbarrier, the others block on a hardware named barrier (no issue slots).
+__device__ __forceinline__ void epi_wait(uint32_t bar, uint32_t parity, int tid, int first) {
+  if (tid == first) mbar_wait(bar, parity);
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+// ... and release it once every thread's TMEM loads completed: one arrive (count 1).
+__device__ __forceinline__ void epi_release_local(uint32_t bar, int tid, int first) {
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (tid == first) mbar_arrive(bar);
+}
 
 // ------------------------------------------------------------------ fused a7 (forward)
 // DOWN epilogue destination of a row: the group's `out` buffer, or — fused forward — the leg's
@@ -210,7 +237,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
     s_pre[nq] = acc;
     s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES + s]), 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(smem_u32(&bars[2 * STAGES + a]), 1); mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(smem_u32(&bars[2 * STAGES + a]), 1); mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&tmA);
   }
@@ -283,7 +310,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
     for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
       int q, m, nb;
       sc.decode(t, q, m, nb);
-      mbar_wait(smem_u32(&bars[2 * STAGES + acc]), acc_phase);
+      epi_wait(smem_u32(&bars[2 * STAGES + acc]), acc_phase, tid, 128);
       tc_fence_after();
       const int row = m * BM + ew * 32 + lane;
       const bool valid = row < s_n[q];
@@ -326,7 +353,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
         if (args.fuse && valid) down_row_done(args, dc, leg, nb, BN, s_fwd);
       }
       tc_fence_before();
-      mbar_arrive(smem_u32(&bars[2 * STAGES + 2 + acc]));
+      epi_release_local(smem_u32(&bars[2 * STAGES + 2 + acc]), tid, 128);
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
   }
@@ -446,7 +473,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     for (int s = 0; s < STAGES2; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES2 + s]), 1); }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
-      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 8);     // 4 epilogue warps x 2 CTAs
+      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 2);     // one arrive per CTA of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&tmA);
@@ -517,7 +544,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     for (int t = cl; t < sc.total; t += ncl) {
       int q, m, nb;
       sc.decode(t, q, m, nb);
-      mbar_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase);
+      epi_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase, tid, 128);
       tc_fence_after();
       const int row = m * BM2 + (int)crank * 128 + ew * 32 + lane;
       const bool valid = row < s_n[q];
@@ -561,7 +588,8 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tid == 128) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
   }
