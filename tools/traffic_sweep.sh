@@ -1,0 +1,4 @@
+for v in 1cta:2048 1cta:8192 2cta:2048 2cta:8192 2cta:32768; do
+  echo "== $v"
+  timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_bytes.sum,smsp__inst_executed.sum,gpu__time_duration.sum -k regex:ffn_tc -s 6 -c 2 python tools/ffn_micro.py --secs 0.5 --variants $v 2>&1 | grep -E "dram__|lts__|inst_exec|duration" 
+done
