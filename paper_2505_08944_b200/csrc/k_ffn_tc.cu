@@ -33,6 +33,7 @@ constexpr int GROUP_M = 16;
 // selects the 1-CTA kernel (UMMA M=128), which also serves d % 256 != 0
 constexpr bool kDefault1Cta = false;
 constexpr uint32_t kSuspendNs = 0x10000;   // mbarrier try_wait suspend-time hint (ns)
+constexpr bool kDefaultL2Hint = false;       // AMOE_L2HINT=1: TMA L2 eviction-priority hints
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;   // + barriers/tile tables + align
 
@@ -47,6 +48,7 @@ struct FfnArgs {
   int32_t w_which;       // 0 (W1; W3 = +1) or 2 (W2) within a queue's 3 tensor maps
   int32_t group_m;       // M tiles per raster group (L2 reuse of the weight slab)
   int32_t fuse;          // DOWN: 1 = store rows straight into the home token pools (fused a7)
+  int32_t l2hint;        // 1 = TMA loads carry L2 evict_last (tokens) / evict_first (weights)
   const amoe_leg* meta;  // [rows] drained legs (fused forward)
   const int32_t* qinfo;
   const CUtensorMap* wmaps;
@@ -84,6 +86,26 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+// Same load with an L2 eviction-priority policy (createpolicy): token rows are re-read for every
+// N tile of their raster group (keep: evict_last); a weight slab is consumed by the group's
+// concurrently running M tiles and then dead until the next group (evict_first).
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" :: "l"(tmap) : "memory");
@@ -256,6 +278,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
   if (warp == 0 && lane == 0) {
     // ===================== TMA producer
     int stage = 0; uint32_t phase = 0;
+    const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
     for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
       int q, m, nb;
       sc.decode(t, q, m, nb);
@@ -267,14 +290,24 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
         const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
         const uint32_t sb = sa + A_BYTES;
         mbar_expect_tx(full, A_BYTES + BN * BK * 2);
-        tma_load_2d(sa, &tmA, kb * BK, arow, full);
-        if (MODE == MODE_GATEUP) {
-          tma_load_2d(sb, wb, kb * BK, nb * 128, full);
-          tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
-        } else {
-          // weight maps have 128-row boxes: BN = 256 takes two loads
+        if (args.l2hint) {
+          tma_load_2d_hint(sa, &tmA, kb * BK, arow, full, pol_a);
 #pragma unroll
-          for (int h = 0; h < BN / 128; ++h) tma_load_2d(sb + h * 128 * BK * 2, wb, kb * BK, nb * BN + h * 128, full);
+          for (int h = 0; h < BN / 128; ++h) {
+            const CUtensorMap* m2 = (MODE == MODE_GATEUP) ? wb + h : wb;
+            const int r0 = (MODE == MODE_GATEUP) ? nb * 128 : nb * BN + h * 128;
+            tma_load_2d_hint(sb + h * 128 * BK * 2, m2, kb * BK, r0, full, pol_b);
+          }
+        } else {
+          tma_load_2d(sa, &tmA, kb * BK, arow, full);
+          if (MODE == MODE_GATEUP) {
+            tma_load_2d(sb, wb, kb * BK, nb * 128, full);
+            tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
+          } else {
+            // weight maps have 128-row boxes: BN = 256 takes two loads
+#pragma unroll
+            for (int h = 0; h < BN / 128; ++h) tma_load_2d(sb + h * 128 * BK * 2, wb, kb * BK, nb * BN + h * 128, full);
+          }
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
@@ -404,6 +437,13 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap,
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const void* tmap, int c0, int c1,
+                                                      uint32_t bar_cluster, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy) : "memory");
+}
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
@@ -495,6 +535,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
     // the leader's full barrier
     int stage = 0; uint32_t phase = 0;
+    const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
     for (int t = cl; t < sc.total; t += ncl) {
       int q, m, nb;
       sc.decode(t, q, m, nb);
@@ -507,8 +548,13 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
         const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
         const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
         if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
-        tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
-        tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
+        if (args.l2hint) {
+          tma_load_2d_pair_hint(sa, &tmA, kb * BK, arow, full_leader, pol_a);
+          tma_load_2d_pair_hint(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader, pol_b);
+        } else {
+          tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
+          tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
+        }
         if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
       }
     }
@@ -640,6 +686,8 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const char* eg = getenv("AMOE_GROUP_M");
   const int gm_rows = eg ? atoi(eg) : 2048;
   a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
+  const char* eh = getenv("AMOE_L2HINT");
+  a.l2hint = eh ? (eh[0] == '1') : kDefaultL2Hint;
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
     a.n_tiles = c.ff / 128;
