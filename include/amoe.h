@@ -202,6 +202,13 @@ amoe_status amoe_expert_ffn(amoe_ctx_t ctx, const amoe_group* grp, void* stream)
  * mode runs amoe_expert_ffn then the amoe_forward kernel. */
 amoe_status amoe_expert_ffn_forward(amoe_ctx_t ctx, const amoe_group* grp, void* stream);
 
+/* a4 + a5 + a6 + a7 fused (what amoe_run uses): drain the group's queues, then the expert FFN
+ * with the re-batch gather inside the gate/up GEMM's A-operand load (TMA tile::gather4 of the
+ * tokens' x rows by slot; the drained legs are read from the rings) and the forward inside the
+ * down GEMM's epilogue. grp->tile/meta/out are not written. Single GPU, bf16; otherwise it runs
+ * amoe_rebatch + amoe_expert_ffn_forward. */
+amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t ctx, const amoe_group* grp, int max_tokens, void* stream);
+
 /* a7 (return leg): store out rows into pool[home][token_slot][k] (NVLink store when remote),
  * bump the token's leg counter (release, system scope); the leg completing K (+S) appends the
  * token to its home's combine ring. */

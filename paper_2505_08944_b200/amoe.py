@@ -73,6 +73,7 @@ EXPORTS = {
     "amoe_expert_ffn": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
     "amoe_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
     "amoe_expert_ffn_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
+    "amoe_rebatch_ffn_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_int, C.c_void_p]),
     "amoe_combine": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "amoe_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, C.POINTER(RunStats), C.c_void_p]),
     "amoe_pass_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(RunParams),
@@ -292,6 +293,10 @@ class Context:
 
     def expert_ffn_forward(self, gb: GroupBuffers, stream=None):
         self._chk(self.lib.amoe_expert_ffn_forward(self.h, C.byref(gb.g), _stream(stream)), "amoe_expert_ffn_forward")
+
+    def rebatch_ffn_forward(self, gb: GroupBuffers, max_tokens=0, stream=None):
+        self._chk(self.lib.amoe_rebatch_ffn_forward(self.h, C.byref(gb.g), max_tokens, _stream(stream)),
+                  "amoe_rebatch_ffn_forward")
 
     def forward(self, gb: GroupBuffers, stream=None):
         self._chk(self.lib.amoe_forward(self.h, C.byref(gb.g), _stream(stream)), "amoe_forward")

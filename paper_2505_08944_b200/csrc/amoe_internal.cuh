@@ -108,6 +108,12 @@ __device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t* p, uint32_t v, boo
   else     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ uint32_t atom_add_release(uint32_t* p, uint32_t v, bool sys) {
+  uint32_t old;
+  if (sys) asm volatile("atom.release.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  else     asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v, bool sys) {
   if (sys) asm volatile("red.release.sys.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
   else     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
@@ -172,10 +178,13 @@ __device__ __forceinline__ uint32_t pieces_per_token(const DevCtx& c) { return (
 __device__ __forceinline__ void leg_pieces_done(const DevCtx& c, int home, int slot, int k, uint32_t pieces) {
   const bool sys = c.G > 1;
   uint32_t* cnt = reinterpret_cast<uint32_t*>(c.peer[home] + c.lay.legs_done) + slot;
-  const uint32_t old = atom_add_acqrel(cnt, pieces, sys);
+  // release-only increment (an acq_rel RMW costs a MEMBAR + L1 invalidate per piece); only the
+  // completing arrival needs the acquire side, which it takes with a fence before publishing
+  const uint32_t old = atom_add_release(cnt, pieces, sys);
   const uint32_t total = pieces_per_token(c);
   if (old + pieces > total) raise_fault(c, F_LEG_OVERCOUNT, slot, old + pieces, k);
   if (old + pieces == total) {
+    fence_sc(sys);
     uint32_t* cctr = reinterpret_cast<uint32_t*>(c.peer[home] + c.lay.cctr);
     amoe_leg* cring = reinterpret_cast<amoe_leg*>(c.peer[home] + c.lay.cring);
     const uint32_t pos = atom_add_relaxed(cctr, 1u, sys);

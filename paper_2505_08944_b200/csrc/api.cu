@@ -22,7 +22,7 @@ int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, const amoe_leg*,
-                  int, int, cudaStream_t, int);
+                  int, int, int, cudaStream_t, int);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
 int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
 }  // namespace amoe
@@ -433,8 +433,10 @@ amoe_status amoe_rebatch(amoe_ctx_t c, const amoe_group* g, int max_tokens, void
   return AMOE_OK;
 }
 
-// a5 + a6 (+ a7 when fuse: the down-GEMM epilogue stores rows straight into the home pools)
-static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaStream_t s) {
+// a5 + a6 (+ a7 when fuse: the down-GEMM epilogue stores rows straight into the home pools;
+// + the a4 gather when gathered: A rows are TMA-gathered from x by token slot, legs read from
+// the rings — single GPU, bf16)
+static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaStream_t s, int gathered = 0) {
   GroupDev gd;
   int wslot[AMOE_MAX_GROUP];
   amoe_status st = make_group(c, g, 0, &gd, wslot);
@@ -445,7 +447,8 @@ static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaSt
   for (int r = 0; r < c->cfg.G; ++r)
     if (fuse && !c->dc.peer[r]) return AMOE_EPEER;
   if (c->cfg.dtype == AMOE_BF16) {
-    const CUtensorMap* mt = cached_map(c, g->tile, g->rows_cap, c->cfg.d, 128);
+    const CUtensorMap* mt = gathered ? cached_map(c, c->ws + c->lay.x, c->cfg.T_slots, c->cfg.d, 1)
+                                     : cached_map(c, g->tile, g->rows_cap, c->cfg.d, 128);
     const CUtensorMap* ma = cached_map(c, g->act, g->rows_cap, c->cfg.ff, 128);
     if (!mt || !ma) return AMOE_ECUDA;
     FfnLaunch f;
@@ -455,11 +458,11 @@ static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaSt
     for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
     {
       StageTimer tm(c, ST_GATEUP, s);
-      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, 0, c->num_sms, s, 1);
+      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, 0, gathered, c->num_sms, s, 1);
     }
     {
       StageTimer tm(c, ST_DOWN, s);
-      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, fuse, c->num_sms, s, 2);
+      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, fuse, gathered, c->num_sms, s, 2);
     }
   } else {
     {
@@ -486,6 +489,25 @@ amoe_status amoe_expert_ffn(amoe_ctx_t c, const amoe_group* g, void* stream) {
 amoe_status amoe_expert_ffn_forward(amoe_ctx_t c, const amoe_group* g, void* stream) {
   if (!c) return AMOE_EINVAL;
   return expert_ffn(c, g, 1, (cudaStream_t)stream);
+}
+
+amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_tokens, void* stream) {
+  if (!c) return AMOE_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->cfg.G == 1 && c->cfg.dtype == AMOE_BF16) {
+    // a4 drain only; the gather happens inside the gate/up GEMM's A-operand load
+    GroupDev gd;
+    amoe_status st = make_group(c, g, max_tokens, &gd, nullptr);
+    if (st != AMOE_OK) return st;
+    {
+      StageTimer tm(c, ST_REBATCH, s);
+      c->launches += launch_drain(c->dc, gd, s);
+    }
+    return expert_ffn(c, g, 1, s, 1);
+  }
+  amoe_status st = amoe_rebatch(c, g, max_tokens, s);
+  if (st != AMOE_OK) return st;
+  return expert_ffn(c, g, 1, s, 0);
 }
 
 amoe_status amoe_forward(amoe_ctx_t c, const amoe_group* g, void* stream) {
@@ -651,8 +673,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         g.nq = 1;
       }
       const int64_t l0 = c->launches;
-      if ((st = amoe_rebatch(c, &g, 0, s)) != AMOE_OK) return st;
-      if ((st = amoe_expert_ffn_forward(c, &g, s)) != AMOE_OK) return st;
+      if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;
       if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
       rs.kernel_launches += c->launches - l0;
       rs.picks += 1;

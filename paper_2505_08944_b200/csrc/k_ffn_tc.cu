@@ -49,7 +49,9 @@ struct FfnArgs {
   int32_t group_m;       // M tiles per raster group (L2 reuse of the weight slab)
   int32_t fuse;          // DOWN: 1 = store rows straight into the home token pools (fused a7)
   int32_t l2hint;        // 1 = TMA loads carry L2 evict_last (tokens) / evict_first (weights)
-  const amoe_leg* meta;  // [rows] drained legs (fused forward)
+  int32_t ring_legs;     // 1 = the drained legs are read from the µ-queue rings (no meta copy)
+  int32_t gather;        // GATEUP: 1 = A rows gathered from x by token slot (TMA tile::gather4)
+  const amoe_leg* meta;  // [rows] drained legs (fused forward) when !ring_legs
   const int32_t* qinfo;
   const CUtensorMap* wmaps;
   __nv_bfloat16* out;
@@ -106,6 +108,21 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+// TMA tile::gather4: 4 rows (arbitrary row coordinates) x 64 columns into 4 consecutive 128-B
+// rows of a 128-B-swizzled tile (tensor map box {64, 1}; the swizzle follows the smem address,
+// so the rows land exactly where a tiled load would put them — tools/gather4_probe.cu).
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void* tmap, int col, int4 rows, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      :: "r"(dst), "l"(tmap), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_gather4_pair(uint32_t dst, const void* tmap, int col, int4 rows, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      :: "r"(dst), "l"(tmap), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" :: "l"(tmap) : "memory");
@@ -211,16 +228,36 @@ __device__ __forceinline__ void epi_release_local(uint32_t bar, int tid, int fir
 // ------------------------------------------------------------------ fused a7 (forward)
 // DOWN epilogue destination of a row: the group's `out` buffer, or — fused forward — the leg's
 // slot in its home's token pool (local or NVLink peer store), pool[home][slot][k][:].
+// The drained leg of row `row` of queue q: from the materialised meta rows, or (ring_legs) from
+// the µ-queue ring itself — position start[q] + row — when the gather was fused into the A load.
+__device__ __forceinline__ amoe_leg leg_of_row(const FfnArgs& a, const DevCtx& dc, int q, int row, int grow,
+                                               const int* s_start) {
+  if (a.ring_legs) {
+    const amoe_leg* ring = reinterpret_cast<const amoe_leg*>(dc.peer[dc.rank] + dc.lay.rings) +
+                           (uint64_t)(a.wslot[q] / 3) * dc.ring_cap;
+    return ring[((uint32_t)s_start[q] + (uint32_t)row) & dc.ring_mask];
+  }
+  return a.meta[grow];
+}
 template <int MODE>
-__device__ __forceinline__ __nv_bfloat16* down_row_dst(const FfnArgs& a, const DevCtx& dc, int grow, bool valid,
-                                                       amoe_leg& leg) {
+__device__ __forceinline__ __nv_bfloat16* down_row_dst(const FfnArgs& a, const DevCtx& dc, int q, int row, int grow,
+                                                       const int* s_start, bool valid, amoe_leg& leg) {
   if (MODE == MODE_DOWN && a.fuse) {
     if (!valid) return nullptr;
-    leg = a.meta[grow];
+    leg = leg_of_row(a, dc, q, row, grow, s_start);
     return reinterpret_cast<__nv_bfloat16*>(dc.peer[leg.home] + dc.lay.pool) +
            ((uint64_t)leg.token_slot * dc.KS + (uint64_t)leg.k) * dc.d;
   }
   return a.out + (uint64_t)grow * a.out_ld;
+}
+// Token slots of 4 consecutive rows of queue q starting at row r0 (rows >= n use slot 0: their
+// outputs are never stored).
+__device__ __forceinline__ int4 gather_rows(const FfnArgs& a, const DevCtx& dc, int q, int r0, int n,
+                                            const int* s_start) {
+  int v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = (r0 + i < n) ? leg_of_row(a, dc, q, r0 + i, 0, s_start).token_slot : 0;
+  return make_int4(v[0], v[1], v[2], v[3]);
 }
 // After this thread stored its row's columns of N tile nb: count the 128-column pieces
 // (release: the stores happen before), completing arrivals append to the combine ring.
@@ -248,10 +285,13 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
   int* s_n = reinterpret_cast<int*>(tmem_holder + 4);
   int* s_off = s_n + AMOE_MAX_GROUP;
   int* s_pre = s_off + AMOE_MAX_GROUP;   // AMOE_MAX_GROUP + 1
+  int* s_start = s_pre + AMOE_MAX_GROUP + 1;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nq = args.nq;
-  for (int q = tid; q < nq; q += THREADS) { s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; }
+  for (int q = tid; q < nq; q += THREADS) {
+    s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; s_start[q] = args.qinfo[2 * AMOE_MAX_GROUP + q];
+  }
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
@@ -275,8 +315,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
   Sched sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_off, s_pre};
   const int kb_n = args.k_blocks;
 
-  if (warp == 0 && lane == 0) {
-    // ===================== TMA producer
+  if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
+    // ===================== TMA producer (lane 0; the whole warp when A rows are gathered:
+    // lane i issues the tile::gather4 of tile rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
     const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
     for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
@@ -284,11 +325,27 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
       sc.decode(t, q, m, nb);
       const int arow = s_off[q] + m * BM;
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
+      int4 rows4 = make_int4(0, 0, 0, 0);
+      if (MODE == MODE_GATEUP && args.gather) rows4 = gather_rows(args, dc, q, m * BM + lane * 4, s_n[q], s_start);
       for (int kb = 0; kb < kb_n; ++kb) {
-        mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
         const uint32_t full = smem_u32(&bars[stage]);
         const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
         const uint32_t sb = sa + A_BYTES;
+        if (MODE == MODE_GATEUP && args.gather) {
+          if (lane == 0) {
+            mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
+            mbar_expect_tx(full, A_BYTES + BN * BK * 2);
+          }
+          __syncwarp();
+          tma_gather4(sa + lane * 4 * 128, &tmA, kb * BK, rows4, full);
+          if (lane == 0) {
+            tma_load_2d(sb, wb, kb * BK, nb * 128, full);
+            tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          continue;
+        }
+        mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
         mbar_expect_tx(full, A_BYTES + BN * BK * 2);
         if (args.l2hint) {
           tma_load_2d_hint(sa, &tmA, kb * BK, arow, full, pol_a);
@@ -348,7 +405,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
       const int row = m * BM + ew * 32 + lane;
       const bool valid = row < s_n[q];
       amoe_leg leg;
-      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, s_off[q] + row, valid, leg);
+      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, s_off[q] + row, s_start, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
       if (MODE == MODE_GATEUP) {
 #pragma unroll 1
@@ -498,12 +555,15 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   int* s_n = reinterpret_cast<int*>(tmem_holder + 4);
   int* s_off = s_n + AMOE_MAX_GROUP;
   int* s_pre = s_off + AMOE_MAX_GROUP;
+  int* s_start = s_pre + AMOE_MAX_GROUP + 1;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = cluster_rank();
   const bool leader = crank == 0;
   const int nq = args.nq;
-  for (int q = tid; q < nq; q += THREADS) { s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; }
+  for (int q = tid; q < nq; q += THREADS) {
+    s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; s_start[q] = args.qinfo[2 * AMOE_MAX_GROUP + q];
+  }
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
@@ -531,9 +591,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   const int kb_n = args.k_blocks;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
     // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
-    // the leader's full barrier
+    // the leader's full barrier (whole warp when A rows are gathered: lane i -> rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
     const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
     for (int t = cl; t < sc.total; t += ncl) {
@@ -543,10 +603,24 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
       const CUtensorMap* bmap = (MODE == MODE_GATEUP) ? wb + crank : wb;
       const int brow = (MODE == MODE_GATEUP) ? nb * 128 : nb * 256 + (int)crank * 128;
+      int4 rows4 = make_int4(0, 0, 0, 0);
+      if (MODE == MODE_GATEUP && args.gather)
+        rows4 = gather_rows(args, dc, q, m * BM2 + (int)crank * 128 + lane * 4, s_n[q], s_start);
       for (int kb = 0; kb < kb_n; ++kb) {
-        mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
         const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
         const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
+        if (MODE == MODE_GATEUP && args.gather) {
+          if (lane == 0) {
+            mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
+            if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
+          }
+          __syncwarp();
+          tma_gather4_pair(sa + lane * 4 * 128, &tmA, kb * BK, rows4, full_leader);
+          if (lane == 0) tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
+          continue;
+        }
+        mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
         if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
         if (args.l2hint) {
           tma_load_2d_pair_hint(sa, &tmA, kb * BK, arow, full_leader, pol_a);
@@ -595,7 +669,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       const int row = m * BM2 + (int)crank * 128 + ew * 32 + lane;
       const bool valid = row < s_n[q];
       amoe_leg leg;
-      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, s_off[q] + row, valid, leg);
+      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, s_off[q] + row, s_start, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
       if (MODE == MODE_GATEUP) {
 #pragma unroll 1
@@ -660,8 +734,11 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
 
 
 // part 1: gate/up + SwiGLU -> act; part 2: down -> out, or (fuse) straight into the home pools.
+// gathered: A rows of part 1 come from x by token slot (tm_tile is then the x map, box {64, 1})
+// and both parts read the drained legs from the rings (no gather kernel, no meta copy).
 int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_tile, const CUtensorMap& tm_act,
-                  void* act, void* out, const amoe_leg* meta, int fuse, int num_sms, cudaStream_t s, int part) {
+                  void* act, void* out, const amoe_leg* meta, int fuse, int gathered, int num_sms, cudaStream_t s,
+                  int part) {
   using namespace tc;
   static bool attr_done = false;
   if (!attr_done) {
@@ -677,6 +754,8 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.qinfo = f.qinfo;
   a.wmaps = f.wmaps;
   a.meta = meta;
+  a.ring_legs = gathered;
+  a.gather = (part == 1) ? gathered : 0;
   for (int q = 0; q < f.nq; ++q) a.wslot[q] = f.wslot[q];
   // CTA-pair kernels need d % 256 == 0 and an even grid; AMOE_FFN_1CTA=1 forces 1-CTA, =0 pairs
   const char* ev = getenv("AMOE_FFN_1CTA");

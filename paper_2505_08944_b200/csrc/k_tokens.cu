@@ -12,7 +12,8 @@ constexpr int kTokThreads = 256;
 constexpr int kTokWarps = kTokThreads / kWarp;
 constexpr int kTPW = 4;                       // tokens per warp per chunk
 constexpr int kTPC = kTokWarps * kTPW;        // tokens per CTA chunk
-constexpr int kU = 4;                         // 16-byte chunks per lane batched in the merge
+constexpr int kU = 2;                         // 16-byte chunks per lane batched in the merge
+constexpr int kCombineMinBlocks = 3;          // register cap (<= 85) for occupancy (ncu: 128 regs -> 25 %)
 
 struct PendingLeg {
   int32_t r;      // owner rank (-1 = inactive)
@@ -255,7 +256,7 @@ __global__ void cdrain_kernel(DevCtx c) {
 // ---------------------------------------------------------------------------- combine (a8)
 
 template <typename T>
-__global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int retire_pass) {
+__global__ void __launch_bounds__(kTokThreads, kCombineMinBlocks) combine_kernel(DevCtx c, int retire_pass) {
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   __shared__ unsigned long long s_merged, s_retired;

@@ -115,6 +115,44 @@ def test_fused_forward_equals_separate_forward(pair):
     assert m0 == m1 == P.T and l0 == l1 == P.T * P.K
 
 
+@pytest.mark.parametrize("pair,d,S", [("0", 512, 0), ("1", 512, 0), ("1", 2048, 2)])
+def test_fused_gather_equals_materialised_gather(pair, d, S):
+    """amoe_rebatch_ffn_forward (gather inside the gate/up A load via TMA tile::gather4, legs read
+    from the rings, forward inside the down epilogue) == rebatch + expert_ffn + forward, bitwise:
+    same pool rows, same merged tokens, same counts; ragged queue tails included."""
+    P = Problem(L=2, E=8, K=2, S=S, d=d, ff=1408 if d == 2048 else 1024, T=1000, seed=15)
+    os.environ["AMOE_FFN_1CTA"] = "1" if pair == "0" else "0"
+    try:
+        res = []
+        for fused in (False, True):
+            ctx = P.make_ctx()
+            from paper_2505_08944_b200 import amoe
+            slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
+            ctx.token_init(slots, dev_tensor(P.h0[0], P.dtype), 0)
+            ctx.enqueue(0, slots, logits=torch.from_numpy(np.ascontiguousarray(P.tables[0][0, 0])).cuda())
+            gb = amoe.GroupBuffers(ctx, P.T * (P.K + P.S) + 128 * (P.E + P.S))
+            gb.set_queues([(0, e) for e in range(P.E + P.S)])
+            if fused:
+                ctx.rebatch_ffn_forward(gb)
+            else:
+                ctx.rebatch(gb)
+                ctx.expert_ffn(gb)
+                ctx.forward(gb)
+            torch.cuda.synchronize()
+            ctx.check()
+            pool = to_np(ctx.state()["pool"]).copy()
+            ctx.combine(retire_pass=1)
+            torch.cuda.synchronize()
+            ctx.check()
+            st = ctx.state()
+            res.append((pool, to_np(st["h"]), int(st["stats"][0])))
+    finally:
+        os.environ.pop("AMOE_FFN_1CTA")
+    (p0, h0, m0), (p1, h1, m1) = res
+    assert m0 == m1 == P.T
+    assert np.array_equal(p0, p1) and np.array_equal(h0, h1)
+
+
 @pytest.mark.slow
 def test_mixtral_layer_fullsize_sampled():
     P = Problem(L=1, E=8, K=2, S=0, d=4096, ff=14336, T=16384, seed=12, n_tab=1)
