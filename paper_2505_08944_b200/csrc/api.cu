@@ -494,7 +494,12 @@ amoe_status amoe_expert_ffn_forward(amoe_ctx_t c, const amoe_group* g, void* str
 amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_tokens, void* stream) {
   if (!c) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (c->cfg.G == 1 && c->cfg.dtype == AMOE_BF16) {
+  // The fused gather is correct (tests) but slower on B200: each A row is re-read by every N tile
+  // of its raster group and TMA tile::gather4 moves ~6.6 B/cycle/SM vs >40 for tiled loads
+  // (profiles/r01_fused_gather.md), so the materialised gather (2·d bytes per leg, once) wins.
+  // Opt in with AMOE_FUSED_GATHER=1.
+  const char* fg = getenv("AMOE_FUSED_GATHER");
+  if (fg && fg[0] == '1' && c->cfg.G == 1 && c->cfg.dtype == AMOE_BF16) {
     // a4 drain only; the gather happens inside the gate/up GEMM's A-operand load
     GroupDev gd;
     amoe_status st = make_group(c, g, max_tokens, &gd, nullptr);

@@ -122,6 +122,7 @@ def test_fused_gather_equals_materialised_gather(pair, d, S):
     same pool rows, same merged tokens, same counts; ragged queue tails included."""
     P = Problem(L=2, E=8, K=2, S=S, d=d, ff=1408 if d == 2048 else 1024, T=1000, seed=15)
     os.environ["AMOE_FFN_1CTA"] = "1" if pair == "0" else "0"
+    os.environ["AMOE_FUSED_GATHER"] = "1"
     try:
         res = []
         for fused in (False, True):
@@ -148,6 +149,7 @@ def test_fused_gather_equals_materialised_gather(pair, d, S):
             res.append((pool, to_np(st["h"]), int(st["stats"][0])))
     finally:
         os.environ.pop("AMOE_FFN_1CTA")
+        os.environ.pop("AMOE_FUSED_GATHER")
     (p0, h0, m0), (p1, h1, m1) = res
     assert m0 == m1 == P.T
     assert np.array_equal(p0, p1) and np.array_equal(h0, h1)
