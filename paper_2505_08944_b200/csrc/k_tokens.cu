@@ -12,8 +12,10 @@ constexpr int kTokThreads = 256;
 constexpr int kTokWarps = kTokThreads / kWarp;
 constexpr int kTPW = 4;                       // tokens per warp per chunk
 constexpr int kTPC = kTokWarps * kTPW;        // tokens per CTA chunk
-constexpr int kU = 2;                         // 16-byte chunks per lane batched in the merge
-constexpr int kCombineMinBlocks = 3;          // register cap (<= 85) for occupancy (ncu: 128 regs -> 25 %)
+// 16-byte chunks per lane batched in the merge. 1 keeps the kernel at ~48 registers (~40 resident
+// warps/SM); measured on B200: kU = 4 (128 regs) and kU = 2 with a register cap (spills) were
+// both slower (Mixtral combine 225 -> 268 -> 458 us/layer): parallelism comes from warps.
+constexpr int kU = 1;
 
 struct PendingLeg {
   int32_t r;      // owner rank (-1 = inactive)
@@ -128,15 +130,15 @@ template <typename T>
 __device__ __forceinline__ void rmsnorm_row(const DevCtx& c, const T* h, T* x, float ss, int lane) {
   using V = Vec<T>;
   const float r = 1.0f / sqrtf(ss / (float)c.d + c.eps);
-  for (int col0 = lane * V::N; col0 < c.d; col0 += 4 * kWarp * V::N) {
-    float f[4][V::N];
+  for (int col0 = lane * V::N; col0 < c.d; col0 += kU * kWarp * V::N) {
+    float f[kU][V::N];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int col = col0 + u * kWarp * V::N;
       if (col < c.d) V::load(h + col, f[u]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int col = col0 + u * kWarp * V::N;
       if (col < c.d) {
 #pragma unroll
@@ -256,7 +258,7 @@ __global__ void cdrain_kernel(DevCtx c) {
 // ---------------------------------------------------------------------------- combine (a8)
 
 template <typename T>
-__global__ void __launch_bounds__(kTokThreads, kCombineMinBlocks) combine_kernel(DevCtx c, int retire_pass) {
+__global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int retire_pass) {
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   __shared__ unsigned long long s_merged, s_retired;
