@@ -14,6 +14,8 @@ namespace amoe {
 constexpr int kWarp = 32;
 constexpr int kMaxKS = 12;          // K + S legs per token
 constexpr int kRowAlign = 128;      // group rows are allocated per queue in multiples of this
+constexpr int kSplitSlots = 512;    // split-K tile slots (counters)
+constexpr int kSplitUnits = 496;    // split-K partial tiles (128 x 256 fp32 each): 62 MB
 
 // Device fault codes latched into the error word.
 enum Fault : uint32_t {
@@ -39,6 +41,7 @@ struct Layout {
   uint64_t cctr;       // u32[4]: combine ring reserve, commit, head, pad
   uint64_t cring;      // amoe_leg[cring_cap]
   uint64_t cinfo;      // i32[4]: combine drain n, start
+  uint64_t split_cnt;  // u32[kSplitSlots]: split-K arrival counters (self-resetting)
   uint64_t h, x;       // [T][d]
   uint64_t pool;       // [T][K+S][d]
   uint64_t legs_done;  // u32[T]
@@ -49,6 +52,7 @@ struct Layout {
   uint64_t wmaps;      // CUtensorMap[L*H][3]
   uint64_t wptrs;      // u64[L*H][3]
   uint64_t s_tile, s_meta, s_qinfo, s_act, s_out;   // amoe_run's group scratch
+  uint64_t split_part; // f32 split-K partials: kSplitUnits x 128 rows x 256 columns
   uint64_t total;
   int32_t rows_cap;
   int32_t pad_;

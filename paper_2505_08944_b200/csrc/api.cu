@@ -177,6 +177,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->rings = take((uint64_t)c->L * H * rc * 16);
   L->cring = take((uint64_t)crc * 16);
   L->cinfo = take(16);
+  L->split_cnt = take((uint64_t)kSplitSlots * 4);
   L->h = take(T * d * es);
   L->x = take(T * d * es);
   L->pool = take(T * KS * d * es);
@@ -192,6 +193,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->s_tile = take((uint64_t)rows * d * es, 1024);
   L->s_act = take((uint64_t)rows * ff * es, 1024);
   L->s_out = take((uint64_t)rows * d * es, 1024);
+  L->split_part = take((uint64_t)kSplitUnits * 128 * 256 * 4, 1024);
   L->total = al(o, 256);
   L->rows_cap = rows;
   *Hr_out = Hr;

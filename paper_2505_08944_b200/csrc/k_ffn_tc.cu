@@ -51,6 +51,9 @@ struct FfnArgs {
   int32_t l2hint;        // 1 = TMA loads carry L2 evict_last (tokens) / evict_first (weights)
   int32_t ring_legs;     // 1 = the drained legs are read from the µ-queue rings (no meta copy)
   int32_t gather;        // GATEUP: 1 = A rows gathered from x by token slot (TMA tile::gather4)
+  int32_t allow_split;   // split K when the output tiles cannot fill the machine (cold experts)
+  float* part;           // split-K fp32 partials (workspace)
+  uint32_t* cnt;         // split-K per-slot arrival counters (workspace, self-resetting)
   const amoe_leg* meta;  // [rows] drained legs (fused forward) when !ring_legs
   const int32_t* qinfo;
   const CUtensorMap* wmaps;
@@ -250,6 +253,120 @@ __device__ __forceinline__ __nv_bfloat16* down_row_dst(const FfnArgs& a, const D
   }
   return a.out + (uint64_t)grow * a.out_ld;
 }
+// ------------------------------------------------------------------ epilogue (shared by both kernels)
+// Final stores of one row of one unit from a value source src(col0, v[32]) — TMEM loads, or the
+// fixed-order sum of split-K partials. GATEUP: act = bf16(silu(g)·u); DOWN: out/pool = bf16(v)
+// (+ fused forward). src must be called by all 32 lanes (tcgen05.ld is warp-collective).
+template <int MODE, int BN, typename Src>
+__device__ __forceinline__ void store_row(const FfnArgs& args, const DevCtx& dc, Src src, bool valid,
+                                          __nv_bfloat16* orow, int nb, const amoe_leg& leg, unsigned long long* s_fwd) {
+  if (MODE == MODE_GATEUP) {
+#pragma unroll 1
+    for (int ch = 0; ch < 4; ++ch) {
+      float g[32], u[32];
+      src(ch * 32, g);
+      src(128 + ch * 32, u);
+      if (valid) {
+        uint4 pk[4];
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          p2[j] = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
+        uint4* dst = reinterpret_cast<uint4*>(orow + nb * 128 + ch * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int ch = 0; ch < BN / 32; ++ch) {
+      float v[32];
+      src(ch * 32, v);
+      const int col = nb * BN + ch * 32;
+      if (valid && col < args.out_cols) {
+        uint4 pk[4];
+        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) p2[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        uint4* dst = reinterpret_cast<uint4*>(orow + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+      }
+    }
+    if (args.fuse && valid) down_row_done(args, dc, leg, nb, BN, s_fwd);
+  }
+}
+
+// Split-K (cold experts: fewer output tiles than SMs): a unit (tile, ks) covers K blocks
+// [ks·kb/split, (ks+1)·kb/split). Its fp32 partial rows go to part[(slot·split + ks)·128 + r];
+// the unit that completes the tile's count sums the partials in ks order (deterministic,
+// independent of arrival order) and runs the final stores.
+template <int MODE, int BN, typename Release>
+__device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, int split, int ks,
+                                              int slot, int rloc, bool valid, __nv_bfloat16* orow, int nb,
+                                              const amoe_leg& leg, unsigned long long* s_fwd, volatile int* s_last,
+                                              int tid, Release release) {
+  auto tmem_src = [&](int col0, float* v) { tmem_ld32(taddr + col0, v); };
+  if (split <= 1) {
+    store_row<MODE, BN>(args, dc, tmem_src, valid, orow, nb, leg, s_fwd);
+    tc_fence_before();
+    release();
+    return;
+  }
+  constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;      // fp32 columns per partial row
+  float* mine = args.part + ((size_t)(slot * split + ks) * 128 + rloc) * W;
+#pragma unroll 1
+  for (int c0 = 0; c0 < W; c0 += 32) {
+    float v[32];
+    tmem_ld32(taddr + c0, v);
+    if (valid) {
+      float4* d4 = reinterpret_cast<float4*>(mine + c0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  }
+  tc_fence_before();
+  release();                       // TMEM free: the MMA proceeds with the next unit
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (tid == 128) {
+    const uint32_t old = atomicAdd(args.cnt + slot, 1u);
+    const int last = old == (uint32_t)(split - 1);
+    if (last) args.cnt[slot] = 0;  // every other unit of this slot already counted
+    *s_last = last;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (!*s_last) return;
+  __threadfence();
+  const float* base = args.part + ((size_t)slot * split * 128 + rloc) * W;
+  auto part_src = [&](int col0, float* v) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    if (!valid) return;
+    for (int s = 0; s < split; ++s) {
+      const float4* p4 = reinterpret_cast<const float4*>(base + (size_t)s * 128 * W + col0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 t = p4[j];
+        v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
+      }
+    }
+  };
+  store_row<MODE, BN>(args, dc, part_src, valid, orow, nb, leg, s_fwd);
+}
+
+// Device-side split decision (identical in every CTA): split K only when the output tiles
+// cannot occupy the tile slots (CTAs or CTA pairs); >= 4 K blocks per unit, <= 2 units per slot.
+// halves = split-K slots per tile (2 for a CTA pair: each CTA reduces its own 128 rows).
+__device__ __forceinline__ int choose_split(const FfnArgs& a, int tiles, int slots, int halves) {
+  if (!a.allow_split || tiles <= 0 || tiles >= slots || tiles * halves > kSplitSlots) return 1;
+  int s = (2 * slots + tiles - 1) / tiles;
+  s = min(s, a.k_blocks / 4);
+  s = min(s, 32);
+  s = min(s, kSplitUnits / (tiles * halves));
+  return max(s, 1);
+}
+
 // Token slots of 4 consecutive rows of queue q starting at row r0 (rows >= n use slot 0: their
 // outputs are never stored).
 __device__ __forceinline__ int4 gather_rows(const FfnArgs& a, const DevCtx& dc, int q, int r0, int n,
@@ -276,6 +393,7 @@ template <int MODE, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];     // legs forwarded, of which remote
+  __shared__ int s_last;                      // split-K: this unit completes its tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -314,20 +432,24 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
   const uint32_t tmem_base = *tmem_holder;
   Sched sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_off, s_pre};
   const int kb_n = args.k_blocks;
+  const int split = choose_split(args, sc.total, gridDim.x, 1);
+  const int units = sc.total * split;
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
     // ===================== TMA producer (lane 0; the whole warp when A rows are gathered:
     // lane i issues the tile::gather4 of tile rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
     const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
-    for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int t = u / split, ks = u - t * split;
       int q, m, nb;
       sc.decode(t, q, m, nb);
       const int arow = s_off[q] + m * BM;
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
       int4 rows4 = make_int4(0, 0, 0, 0);
       if (MODE == MODE_GATEUP && args.gather) rows4 = gather_rows(args, dc, q, m * BM + lane * 4, s_n[q], s_start);
-      for (int kb = 0; kb < kb_n; ++kb) {
+      const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
+      for (int kb = kb0; kb < kb1; ++kb) {
         const uint32_t full = smem_u32(&bars[stage]);
         const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
         const uint32_t sb = sa + A_BYTES;
@@ -374,11 +496,13 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
     constexpr uint32_t idesc = idesc_bf16(BM, BN);
     int stage = 0; uint32_t phase = 0;
     int acc = 0; uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int ks = u % split;
+      const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
       mbar_wait(smem_u32(&bars[2 * STAGES + 2 + acc]), acc_phase ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
-      for (int kb = 0; kb < kb_n; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(smem_u32(&bars[stage]), phase);
         tc_fence_after();
         const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
@@ -386,7 +510,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
         const uint64_t bdesc = umma_desc_sw128(sa + A_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the swizzle atom = +2 in desc units
-          umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0) | (k > 0));
         umma_commit(smem_u32(&bars[STAGES + stage]));     // frees the smem stage when MMAs retire
         if (++stage == STAGES) { stage = 0; phase ^= 1u; }
       }
@@ -397,7 +521,8 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
     // ===================== epilogue: TMEM -> registers -> global
     const int ew = warp - 4;            // TMEM lane quarter (warp % 4)
     int acc = 0; uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int t = u / split, ks = u - t * split;
       int q, m, nb;
       sc.decode(t, q, m, nb);
       epi_wait(smem_u32(&bars[2 * STAGES + acc]), acc_phase, tid, 128);
@@ -407,43 +532,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
       amoe_leg leg;
       __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, s_off[q] + row, s_start, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
-      if (MODE == MODE_GATEUP) {
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          float g[32], u[32];
-          tmem_ld32(taddr + ch * 32, g);
-          tmem_ld32(taddr + 128 + ch * 32, u);
-          if (valid) {
-            uint4 pk[4];
-            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              p2[j] = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
-            uint4* dst = reinterpret_cast<uint4*>(orow + nb * 128 + ch * 32);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
-          float v[32];
-          tmem_ld32(taddr + ch * 32, v);
-          const int col = nb * BN + ch * 32;
-          if (valid && col < args.out_cols) {
-            uint4 pk[4];
-            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) p2[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(orow + col);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
-          }
-        }
-        if (args.fuse && valid) down_row_done(args, dc, leg, nb, BN, s_fwd);
-      }
-      tc_fence_before();
-      epi_release_local(smem_u32(&bars[2 * STAGES + 2 + acc]), tid, 128);
+      const uint32_t tempty = smem_u32(&bars[2 * STAGES + 2 + acc]);
+      epilogue_unit<MODE, BN>(args, dc, taddr, split, ks, t, ew * 32 + lane, valid, orow, nb, leg, s_fwd, &s_last, tid,
+                              [&] { epi_release_local(tempty, tid, 128); });
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
   }
@@ -546,6 +637,7 @@ template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];
+  __shared__ int s_last;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -590,13 +682,17 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   Sched2 sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_pre};
   const int kb_n = args.k_blocks;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int split = choose_split(args, sc.total, ncl, 2);
+  const int units = sc.total * split;
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
     // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
     // the leader's full barrier (whole warp when A rows are gathered: lane i -> rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
     const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
-    for (int t = cl; t < sc.total; t += ncl) {
+    for (int u = cl; u < units; u += ncl) {
+      const int t = u / split, ks = u - t * split;
+      const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
       int q, m, nb;
       sc.decode(t, q, m, nb);
       const int arow = s_off[q] + m * BM2 + (int)crank * 128;
@@ -606,7 +702,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       int4 rows4 = make_int4(0, 0, 0, 0);
       if (MODE == MODE_GATEUP && args.gather)
         rows4 = gather_rows(args, dc, q, m * BM2 + (int)crank * 128 + lane * 4, s_n[q], s_start);
-      for (int kb = 0; kb < kb_n; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
         const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
         if (MODE == MODE_GATEUP && args.gather) {
@@ -637,11 +733,13 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     constexpr uint32_t idesc = idesc_bf16(BM2, 256);
     int stage = 0; uint32_t phase = 0;
     int acc = 0; uint32_t acc_phase = 0;
-    for (int t = cl; t < sc.total; t += ncl) {
+    for (int u = cl; u < units; u += ncl) {
+      const int ks = u % split;
+      const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
       mbar_wait(smem_u32(&bars[2 * STAGES2 + 2 + acc]), acc_phase ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
-      for (int kb = 0; kb < kb_n; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(smem_u32(&bars[stage]), phase);
         tc_fence_after();
         const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
@@ -649,7 +747,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
         const uint64_t bdesc = umma_desc_sw128(sa + HALF_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > kb0) | (k > 0));
         umma_commit_pair(smem_u32(&bars[STAGES2 + stage]));       // frees the stage in both CTAs
         if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
       }
@@ -661,7 +759,8 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     const int ew = warp - 4;
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&bars[2 * STAGES2 + 2]), 0);
-    for (int t = cl; t < sc.total; t += ncl) {
+    for (int u = cl; u < units; u += ncl) {
+      const int t = u / split, ks = u - t * split;
       int q, m, nb;
       sc.decode(t, q, m, nb);
       epi_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase, tid, 128);
@@ -671,45 +770,14 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       amoe_leg leg;
       __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, s_off[q] + row, s_start, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
-      if (MODE == MODE_GATEUP) {
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          float g[32], u[32];
-          tmem_ld32(taddr + ch * 32, g);
-          tmem_ld32(taddr + 128 + ch * 32, u);
-          if (valid) {
-            uint4 pk[4];
-            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              p2[j] = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
-            uint4* dst = reinterpret_cast<uint4*>(orow + nb * 128 + ch * 32);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int ch = 0; ch < 8; ++ch) {
-          float v[32];
-          tmem_ld32(taddr + ch * 32, v);
-          const int col = nb * 256 + ch * 32;
-          if (valid && col < args.out_cols) {
-            uint4 pk[4];
-            __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) p2[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(orow + col);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = pk[j];
-          }
-        }
-        if (args.fuse && valid) down_row_done(args, dc, leg, nb, 256, s_fwd);
-      }
-      tc_fence_before();
-      __syncwarp();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tid == 128) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * 8));
+      const uint32_t tempty = tempty_leader0 + (uint32_t)(acc * 8);
+      // each CTA's half tile is its own split-K slot: 2 t + crank
+      epilogue_unit<MODE, 256>(args, dc, taddr, split, ks, 2 * t + (int)crank, ew * 32 + lane, valid, orow, nb, leg,
+                               s_fwd, &s_last, tid, [&] {
+                                 __syncwarp();
+                                 asm volatile("bar.sync 1, 128;" ::: "memory");
+                                 if (tid == 128) mbar_arrive_cluster(tempty);
+                               });
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
   }
@@ -754,6 +822,10 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.qinfo = f.qinfo;
   a.wmaps = f.wmaps;
   a.meta = meta;
+  a.part = reinterpret_cast<float*>(c.peer[c.rank] + c.lay.split_part);
+  a.cnt = reinterpret_cast<uint32_t*>(c.peer[c.rank] + c.lay.split_cnt);
+  const char* es = getenv("AMOE_SPLITK");
+  a.allow_split = es ? (es[0] == '1') : 1;
   a.ring_legs = gathered;
   a.gather = (part == 1) ? gathered : 0;
   for (int q = 0; q < f.nq; ++q) a.wslot[q] = f.wslot[q];

@@ -155,6 +155,57 @@ def test_fused_gather_equals_materialised_gather(pair, d, S):
     assert np.array_equal(p0, p1) and np.array_equal(h0, h1)
 
 
+@pytest.mark.parametrize("pair,d,ff,T", [("1", 2048, 1408, 40), ("0", 2048, 1408, 40), ("1", 4096, 2048, 100),
+                                         ("1", 2048, 1408, 300)])
+def test_split_k_cold_expert(pair, d, ff, T):
+    """Cold experts (fewer output tiles than SMs) split K across CTAs with a fixed-order fp32
+    reduction by the last arriving unit: outputs meet the oracle gate and stay within two bf16
+    ulps of the unsplit kernels; the fused forward of split tiles returns every leg exactly once."""
+    P = Problem(L=1, E=4, K=1, S=0, d=d, ff=ff, T=T, seed=16)
+    outs = []
+    os.environ["AMOE_FFN_1CTA"] = "1" if pair == "0" else "0"
+    try:
+        for split in ("1", "0"):
+            os.environ["AMOE_SPLITK"] = split
+            ctx = P.make_ctx()
+            gb = _run_layer(P, ctx)
+            n, off, _ = gb.info()
+            outs.append((to_np(gb.tile), to_np(gb.out), gb.meta.cpu().numpy(), n, off))
+            if split == "1":
+                # separate forward + merge vs fused forward (split tiles) + merge: identical tokens
+                ctx.forward(gb)
+                ctx.combine(retire_pass=1)
+                torch.cuda.synchronize()
+                ctx.check()
+                assert int(ctx.state()["stats"][0]) == P.T
+                from paper_2505_08944_b200 import amoe
+                c2 = P.make_ctx()
+                slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
+                c2.token_init(slots, dev_tensor(P.h0[0], P.dtype), 0)
+                c2.enqueue(0, slots, logits=torch.from_numpy(np.ascontiguousarray(P.tables[0][0, 0])).cuda())
+                g2 = amoe.GroupBuffers(c2, P.T * P.K + 128 * P.E).set_queues([(0, e) for e in range(P.E)])
+                c2.rebatch(g2)
+                c2.expert_ffn_forward(g2)
+                c2.combine(retire_pass=1)
+                torch.cuda.synchronize()
+                c2.check()
+                assert int(c2.state()["stats"][0]) == P.T
+                assert np.array_equal(to_np(c2.state()["h"]), to_np(ctx.state()["h"]))
+    finally:
+        os.environ.pop("AMOE_SPLITK", None)
+        os.environ.pop("AMOE_FFN_1CTA", None)
+    (t0, o0, m0, n, off), (t1, o1, m1, n1, off1) = outs
+    for i in range(P.E):
+        if n[i] == 0:
+            continue
+        r0, r1 = slice(off[i], off[i] + n[i]), slice(off1[i], off1[i] + n1[i])
+        ref = nx.expert_ffn(t0[r0], *P.W[(0, i)])
+        assert floored_err(o0[r0], ref) <= 2.0 ** -7, (i, floored_err(o0[r0], ref))
+        k0, k1 = m0[r0, 0], m1[r1, 0]
+        a0, a1 = o0[r0][np.argsort(k0)], o1[r1][np.argsort(k1)]
+        assert floored_err(a0, a1) <= 2.0 ** -6
+
+
 @pytest.mark.slow
 def test_mixtral_layer_fullsize_sampled():
     P = Problem(L=1, E=8, K=2, S=0, d=4096, ff=14336, T=16384, seed=12, n_tab=1)
