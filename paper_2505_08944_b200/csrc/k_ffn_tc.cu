@@ -299,8 +299,8 @@ __device__ __forceinline__ void store_row(const FfnArgs& args, const DevCtx& dc,
 
 // Split-K (cold experts: fewer output tiles than SMs): a unit (tile, ks) covers K blocks
 // [ks·kb/split, (ks+1)·kb/split). Its fp32 partial rows go to part[(slot·split + ks)·128 + r];
-// the unit that completes the tile's count sums the partials in ks order (deterministic,
-// independent of arrival order) and runs the final stores.
+// splitk_reduce_kernel then sums the partials in ks order (deterministic, independent of which
+// unit finished first) and runs the final stores.
 template <int MODE, int BN, typename Release>
 __device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, int split, int ks,
                                               int slot, int rloc, bool valid, __nv_bfloat16* orow, int nb,
@@ -327,32 +327,7 @@ __device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx&
   }
   tc_fence_before();
   release();                       // TMEM free: the MMA proceeds with the next unit
-  __threadfence();
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (tid == 128) {
-    const uint32_t old = atomicAdd(args.cnt + slot, 1u);
-    const int last = old == (uint32_t)(split - 1);
-    if (last) args.cnt[slot] = 0;  // every other unit of this slot already counted
-    *s_last = last;
-  }
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (!*s_last) return;
-  __threadfence();
-  const float* base = args.part + ((size_t)slot * split * 128 + rloc) * W;
-  auto part_src = [&](int col0, float* v) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = 0.f;
-    if (!valid) return;
-    for (int s = 0; s < split; ++s) {
-      const float4* p4 = reinterpret_cast<const float4*>(base + (size_t)s * 128 * W + col0);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float4 t = p4[j];
-        v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
-      }
-    }
-  };
-  store_row<MODE, BN>(args, dc, part_src, valid, orow, nb, leg, s_fwd);
+  // the fixed-order reduction and the final stores run in splitk_reduce_kernel (stream-ordered)
 }
 
 // Device-side split decision (identical in every CTA): split K only when the output tiles
@@ -796,6 +771,104 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
 }
 }  // namespace tc2
 
+// ================================================================== split-K reduction
+// Recomputes the GEMM's (device-side) split decision from the same inputs; a no-op when the GEMM
+// did not split. One warp per valid output row of a split tile: partials summed in ks order
+// (coalesced fp32 loads), then the same final stores as the unsplit epilogue: SwiGLU -> act, or
+// bf16 -> out / home pool + leg-piece count (fused forward).
+template <int MODE, int BN, bool PAIR>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, const __grid_constant__ DevCtx dc,
+                                                            int slots) {
+  constexpr int BMx = PAIR ? 256 : 128;
+  constexpr int HALVES = PAIR ? 2 : 1;
+  constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;        // partial row width (fp32)
+  constexpr int CPL = (MODE == MODE_GATEUP ? 128 : BN) / 32;  // output columns per lane
+  __shared__ int s_n[AMOE_MAX_GROUP], s_off[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP], s_pre[AMOE_MAX_GROUP + 1];
+  const int nq = args.nq;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; s_start[q] = args.qinfo[2 * AMOE_MAX_GROUP + q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BMx - 1) / BMx * args.n_tiles; }
+    s_pre[nq] = acc;
+  }
+  __syncthreads();
+  const int total = s_pre[nq];
+  const int split = choose_split(args, total, slots, HALVES);
+  if (split <= 1) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int items = total * HALVES * 128;
+  for (int it = gw; it < items; it += nw) {
+    const int t = it / (HALVES * 128), rem = it - t * HALVES * 128, h = rem / 128, r = rem - h * 128;
+    int q, m, nb;
+    if (PAIR) tc2::Sched2{nq, args.n_tiles, total, args.group_m, s_n, s_pre}.decode(t, q, m, nb);
+    else Sched{nq, args.n_tiles, total, args.group_m, s_n, s_off, s_pre}.decode(t, q, m, nb);
+    const int row = m * BMx + h * 128 + r;
+    if (row >= s_n[q]) continue;
+    const int slot = PAIR ? 2 * t + h : t;
+    const float* base = args.part + ((size_t)slot * split * 128 + r) * W;
+    const int grow = s_off[q] + row;
+    if (MODE == MODE_GATEUP) {
+      const int c = lane * CPL;
+      float g[CPL], u[CPL];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) { g[j] = 0.f; u[j] = 0.f; }
+      for (int s = 0; s < split; ++s) {
+        const float* p = base + (size_t)s * 128 * W;
+        const float4 a = *reinterpret_cast<const float4*>(p + c);
+        const float4 b = *reinterpret_cast<const float4*>(p + 128 + c);
+        g[0] += a.x; g[1] += a.y; g[2] += a.z; g[3] += a.w;
+        u[0] += b.x; u[1] += b.y; u[2] += b.z; u[3] += b.w;
+      }
+      __nv_bfloat162 o[2];
+      o[0] = __floats2bfloat162_rn(silu_mul(g[0], u[0]), silu_mul(g[1], u[1]));
+      o[1] = __floats2bfloat162_rn(silu_mul(g[2], u[2]), silu_mul(g[3], u[3]));
+      *reinterpret_cast<uint2*>(args.out + (uint64_t)grow * args.out_ld + nb * 128 + c) = *reinterpret_cast<uint2*>(o);
+    } else {
+      const int c = lane * CPL;
+      float v[CPL];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) v[j] = 0.f;
+      for (int s = 0; s < split; ++s) {
+        const float* p = base + (size_t)s * 128 * W + c;
+#pragma unroll
+        for (int j = 0; j < CPL; j += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(p + j);
+          v[j] += a.x; v[j + 1] += a.y; v[j + 2] += a.z; v[j + 3] += a.w;
+        }
+      }
+      amoe_leg leg;
+      __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, grow, s_start, true, leg);
+      const int col = nb * BN + c;
+      if (col < args.out_cols) {
+#pragma unroll
+        for (int j = 0; j < CPL; j += 4) {
+          __nv_bfloat162 o[2];
+          o[0] = __floats2bfloat162_rn(v[j], v[j + 1]);
+          o[1] = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+          *reinterpret_cast<uint2*>(orow + col + j) = *reinterpret_cast<uint2*>(o);
+        }
+      }
+      if (args.fuse) {
+        __syncwarp();
+        if (lane == 0) {
+          fence_sc(dc.G > 1);          // the warp's row stores before the piece count
+          const int cols = min(BN, dc.d - nb * BN);
+          if (cols > 0) leg_pieces_done(dc, leg.home, leg.token_slot, leg.k, (uint32_t)(cols / 128));
+          if (nb == 0) {
+            unsigned long long* st = wsp<unsigned long long>(dc, dc.rank, dc.lay.stats);
+            atomicAdd(st + 2, 1ull);
+            if (leg.home != dc.rank) atomicAdd(st + 3, 1ull);
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace tc
 
 // ------------------------------------------------------------------ launchers
@@ -867,14 +940,27 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (part == 1) cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
-    else cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
-    return 1;
+    const int slots = (num_sms & ~1) / 2;
+    if (part == 1) {
+      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
+      if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
+    } else {
+      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
+      if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
+    }
+    return a.allow_split ? 2 : 1;
   }
-  if (part == 1) ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a, c);
-  else if (bn == 256) ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
-  else ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
-  return 1;
+  if (part == 1) {
+    ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a, c);
+    if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
+  } else if (bn == 256) {
+    ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
+    if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
+  } else {
+    ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
+    if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 128, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
+  }
+  return a.allow_split ? 2 : 1;
 }
 
 }  // namespace amoe
