@@ -21,8 +21,8 @@ int launch_announce(const DevCtx&, uint32_t, cudaStream_t);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
-int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, void*, void*, const amoe_leg*,
-                  int, int, int, cudaStream_t, int);
+int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                  const CUtensorMap&, void*, void*, const amoe_leg*, int, int, int, cudaStream_t, int);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
 int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
 }  // namespace amoe
@@ -449,10 +449,19 @@ static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaSt
   for (int r = 0; r < c->cfg.G; ++r)
     if (fuse && !c->dc.peer[r]) return AMOE_EPEER;
   if (c->cfg.dtype == AMOE_BF16) {
-    const CUtensorMap* mt = gathered ? cached_map(c, c->ws + c->lay.x, c->cfg.T_slots, c->cfg.d, 1)
-                                     : cached_map(c, g->tile, g->rows_cap, c->cfg.d, 128);
-    const CUtensorMap* ma = cached_map(c, g->act, g->rows_cap, c->cfg.ff, 128);
-    if (!mt || !ma) return AMOE_ECUDA;
+    // copies: cached_map returns pointers into a vector that later lookups may reallocate
+    CUtensorMap mt, ma, mt32, ma32;
+    const CUtensorMap* p;
+    if (!(p = gathered ? cached_map(c, c->ws + c->lay.x, c->cfg.T_slots, c->cfg.d, 1)
+                       : cached_map(c, g->tile, g->rows_cap, c->cfg.d, 128))) return AMOE_ECUDA;
+    mt = *p;
+    if (!(p = cached_map(c, g->act, g->rows_cap, c->cfg.ff, 128))) return AMOE_ECUDA;
+    ma = *p;
+    if (!(p = gathered ? cached_map(c, c->ws + c->lay.x, c->cfg.T_slots, c->cfg.d, 1)
+                       : cached_map(c, g->tile, g->rows_cap, c->cfg.d, 32))) return AMOE_ECUDA;
+    mt32 = *p;
+    if (!(p = cached_map(c, g->act, g->rows_cap, c->cfg.ff, 32))) return AMOE_ECUDA;
+    ma32 = *p;
     FfnLaunch f;
     f.nq = g->nq;
     f.qinfo = g->qinfo;
@@ -460,11 +469,12 @@ static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaSt
     for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
     {
       StageTimer tm(c, ST_GATEUP, s);
-      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, 0, gathered, c->num_sms, s, 1);
+      c->launches += launch_ffn_tc(c->dc, f, mt, ma, mt32, ma32, g->act, g->out, g->meta, 0, gathered, c->num_sms, s, 1);
     }
     {
       StageTimer tm(c, ST_DOWN, s);
-      c->launches += launch_ffn_tc(c->dc, f, *mt, *ma, g->act, g->out, g->meta, fuse, gathered, c->num_sms, s, 2);
+      c->launches +=
+          launch_ffn_tc(c->dc, f, mt, ma, mt32, ma32, g->act, g->out, g->meta, fuse, gathered, c->num_sms, s, 2);
     }
   } else {
     {

@@ -333,10 +333,12 @@ __device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx&
 // Device-side split decision (identical in every CTA): split K only when the output tiles
 // cannot occupy the tile slots (CTAs or CTA pairs); >= 4 K blocks per unit, <= 2 units per slot.
 // halves = split-K slots per tile (2 for a CTA pair: each CTA reduces its own 128 rows).
-__device__ __forceinline__ int choose_split(const FfnArgs& a, int tiles, int slots, int halves) {
-  if (!a.allow_split || tiles <= 0 || tiles >= slots || tiles * halves > kSplitSlots) return 1;
-  int s = (2 * slots + tiles - 1) / tiles;
-  s = min(s, a.k_blocks / 4);
+// Only the cold regime splits (every queue fits one M tile: weight streaming dominates and the
+// fp32 partials are small); units keep >= 8 K blocks and aim at ~4 per tile slot.
+__device__ __forceinline__ int choose_split(const FfnArgs& a, int tiles, int slots, int halves, int max_m_tiles) {
+  if (!a.allow_split || tiles <= 0 || max_m_tiles > 1 || tiles >= 2 * slots || tiles * halves > kSplitSlots) return 1;
+  int s = (4 * slots + tiles - 1) / tiles;
+  s = min(s, a.k_blocks / 8);
   s = min(s, 32);
   s = min(s, kSplitUnits / (tiles * halves));
   return max(s, 1);
@@ -366,7 +368,8 @@ __device__ __forceinline__ void down_row_done(const FfnArgs& a, const DevCtx& dc
 
 template <int MODE, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
-ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
+ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA32, const FfnArgs args,
+              const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];     // legs forwarded, of which remote
   __shared__ int s_last;                      // split-K: this unit completes its tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -388,8 +391,12 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
-    for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BM - 1) / BM * args.n_tiles; }
+    int mm = 0;
+    for (int q = 0; q < nq; ++q) {
+      s_pre[q] = acc; acc += (s_n[q] + BM - 1) / BM * args.n_tiles; mm = max(mm, (s_n[q] + BM - 1) / BM);
+    }
     s_pre[nq] = acc;
+    s_start[AMOE_MAX_GROUP] = mm;
     s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES + s]), 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(smem_u32(&bars[2 * STAGES + a]), 1); mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 1); }
@@ -407,7 +414,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
   const uint32_t tmem_base = *tmem_holder;
   Sched sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_off, s_pre};
   const int kb_n = args.k_blocks;
-  const int split = choose_split(args, sc.total, gridDim.x, 1);
+  const int split = choose_split(args, sc.total, gridDim.x, 1, s_start[AMOE_MAX_GROUP]);
   const int units = sc.total * split;
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
@@ -420,6 +427,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
       int q, m, nb;
       sc.decode(t, q, m, nb);
       const int arow = s_off[q] + m * BM;
+      const int rows_valid = s_n[q] - m * BM;
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
       int4 rows4 = make_int4(0, 0, 0, 0);
       if (MODE == MODE_GATEUP && args.gather) rows4 = gather_rows(args, dc, q, m * BM + lane * 4, s_n[q], s_start);
@@ -443,7 +451,10 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
           continue;
         }
         mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
-        mbar_expect_tx(full, A_BYTES + BN * BK * 2);
+        // a partial M tile loads only its valid rows (32-row boxes); the rest of the smem tile
+        // is stale and only feeds accumulator rows that are never stored
+        const int nA = (args.l2hint || rows_valid >= BM) ? 0 : (rows_valid + 31) / 32;
+        mbar_expect_tx(full, (nA ? nA * 32 * BK * 2 : A_BYTES) + BN * BK * 2);
         if (args.l2hint) {
           tma_load_2d_hint(sa, &tmA, kb * BK, arow, full, pol_a);
 #pragma unroll
@@ -453,7 +464,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const
             tma_load_2d_hint(sb + h * 128 * BK * 2, m2, kb * BK, r0, full, pol_b);
           }
         } else {
-          tma_load_2d(sa, &tmA, kb * BK, arow, full);
+          if (nA == 0) tma_load_2d(sa, &tmA, kb * BK, arow, full);
+          else
+            for (int i = 0; i < nA; ++i) tma_load_2d(sa + i * 32 * BK * 2, &tmA32, kb * BK, arow + i * 32, full);
           if (MODE == MODE_GATEUP) {
             tma_load_2d(sb, wb, kb * BK, nb * 128, full);
             tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
@@ -610,7 +623,8 @@ struct Sched2 {
 
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
-ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
+ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA32, const FfnArgs args,
+               const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];
   __shared__ int s_last;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -634,8 +648,12 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   __syncthreads();
   if (tid == 0) {
     int acc = 0;
-    for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BM2 - 1) / BM2 * args.n_tiles; }
+    int mm = 0;
+    for (int q = 0; q < nq; ++q) {
+      s_pre[q] = acc; acc += (s_n[q] + BM2 - 1) / BM2 * args.n_tiles; mm = max(mm, (s_n[q] + BM2 - 1) / BM2);
+    }
     s_pre[nq] = acc;
+    s_start[AMOE_MAX_GROUP] = mm;
     s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES2; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES2 + s]), 1); }
     for (int a = 0; a < 2; ++a) {
@@ -657,7 +675,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   Sched2 sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_pre};
   const int kb_n = args.k_blocks;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int split = choose_split(args, sc.total, ncl, 2);
+  const int split = choose_split(args, sc.total, ncl, 2, s_start[AMOE_MAX_GROUP]);
   const int units = sc.total * split;
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
@@ -692,12 +710,21 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
           continue;
         }
         mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
-        if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
+        // partial M tile: each CTA loads only its valid rows in 32-row boxes (the leader's
+        // expected byte count covers both CTAs' A rows and both B halves)
+        const int rv0 = s_n[q] - m * BM2, rv1 = rv0 - 128;
+        auto a_loads = [&](int rv) { return (args.l2hint || rv >= 128) ? -1 : (rv <= 0 ? 0 : (rv + 31) / 32); };
+        auto a_bytes = [&](int rv) { const int l = a_loads(rv); return l < 0 ? HALF_BYTES : l * 32 * BK * 2; };
+        if (leader) mbar_expect_tx(smem_u32(&bars[stage]), a_bytes(rv0) + a_bytes(rv1) + 2 * HALF_BYTES);
+        const int nA = a_loads(crank ? rv1 : rv0);
         if (args.l2hint) {
           tma_load_2d_pair_hint(sa, &tmA, kb * BK, arow, full_leader, pol_a);
           tma_load_2d_pair_hint(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader, pol_b);
         } else {
-          tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
+          if (nA < 0) tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
+          else
+            for (int i = 0; i < nA; ++i)
+              tma_load_2d_pair(sa + i * 32 * BK * 2, &tmA32, kb * BK, arow + i * 32, full_leader);
           tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
         }
         if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
@@ -784,6 +811,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
   constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;        // partial row width (fp32)
   constexpr int CPL = (MODE == MODE_GATEUP ? 128 : BN) / 32;  // output columns per lane
   __shared__ int s_n[AMOE_MAX_GROUP], s_off[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP], s_pre[AMOE_MAX_GROUP + 1];
+  __shared__ int s_mmax;
   const int nq = args.nq;
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
     s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; s_start[q] = args.qinfo[2 * AMOE_MAX_GROUP + q];
@@ -791,12 +819,16 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
-    for (int q = 0; q < nq; ++q) { s_pre[q] = acc; acc += (s_n[q] + BMx - 1) / BMx * args.n_tiles; }
+    int mm = 0;
+    for (int q = 0; q < nq; ++q) {
+      s_pre[q] = acc; acc += (s_n[q] + BMx - 1) / BMx * args.n_tiles; mm = max(mm, (s_n[q] + BMx - 1) / BMx);
+    }
     s_pre[nq] = acc;
+    s_mmax = mm;
   }
   __syncthreads();
   const int total = s_pre[nq];
-  const int split = choose_split(args, total, slots, HALVES);
+  const int split = choose_split(args, total, slots, HALVES, s_mmax);
   if (split <= 1) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -877,7 +909,9 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
 // part 1: gate/up + SwiGLU -> act; part 2: down -> out, or (fuse) straight into the home pools.
 // gathered: A rows of part 1 come from x by token slot (tm_tile is then the x map, box {64, 1})
 // and both parts read the drained legs from the rings (no gather kernel, no meta copy).
+// tm_*32: the same tensors with 32-row boxes (partial M tiles load only their valid rows).
 int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_tile, const CUtensorMap& tm_act,
+                  const CUtensorMap& tm_tile32, const CUtensorMap& tm_act32,
                   void* act, void* out, const amoe_leg* meta, int fuse, int gathered, int num_sms, cudaStream_t s,
                   int part) {
   using namespace tc;
@@ -942,22 +976,22 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     cfg.numAttrs = 1;
     const int slots = (num_sms & ~1) / 2;
     if (part == 1) {
-      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
+      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, tm_tile32, a, c);
       if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
     } else {
-      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
+      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, tm_act32, a, c);
       if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
     }
     return a.allow_split ? 2 : 1;
   }
   if (part == 1) {
-    ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, a, c);
+    ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, tm_tile32, a, c);
     if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
   } else if (bn == 256) {
-    ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
+    ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, tm_act32, a, c);
     if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
   } else {
-    ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, a, c);
+    ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, tm_act32, a, c);
     if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 128, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
   }
   return a.allow_split ? 2 : 1;

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--shapes", default="mixtral,deepseek")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--grouped", type=int, default=0,
+                    help="also measure G distinct experts with n tokens each in ONE grouped launch "
+                         "(what the Algorithm-1 grouped pick executes for cold layers)")
     args = ap.parse_args()
     import torch
     from paper_2505_08944_b200 import amoe
@@ -78,6 +81,50 @@ def main():
             del gbs
         ctx.close()
         torch.cuda.empty_cache()
+        if args.grouped:
+            Gx = args.grouped
+            cfg = amoe.make_config(2, Gx, 1, 0, d, ff, Gx * 256)
+            ctx = amoe.Context(cfg)
+            for l in range(2):
+                for e in range(Gx):
+                    ctx.set_expert(l, e, torch.randn(ff, d, device="cuda", dtype=torch.bfloat16) * d ** -0.5,
+                                   torch.randn(ff, d, device="cuda", dtype=torch.bfloat16) * d ** -0.5,
+                                   torch.randn(d, ff, device="cuda", dtype=torch.bfloat16) * ff ** -0.5)
+            h0 = torch.randn(Gx * 256, d, device="cuda", dtype=torch.bfloat16)
+            for n in [x for x in NS if x <= 256]:
+                nt = n * Gx
+                slots = torch.arange(nt, dtype=torch.int32, device="cuda")
+                idx = (torch.arange(nt, device="cuda", dtype=torch.int32) % Gx).view(nt, 1)
+                gbs = []
+                for l in range(2):
+                    ctx.token_init(slots, h0[:nt])
+                    ctx.enqueue(l, slots, topk_idx=idx, topk_w=torch.ones(nt, 1, device="cuda"))
+                    gb = amoe.GroupBuffers(ctx, Gx * ((n + 255) // 256) * 256).set_queues([(l, e) for e in range(Gx)])
+                    ctx.rebatch(gb)
+                    gbs.append(gb)
+                for gb in gbs:
+                    ctx.expert_ffn(gb)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(args.iters):
+                    for gb in gbs:
+                        ctx.expert_ffn(gb)
+                e1.record()
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 1e3 / (args.iters * 2)
+                flop = 6.0 * d * ff * nt
+                wbytes = 6.0 * d * ff * Gx
+                roof = max(flop / tc, (wbytes + 4.0 * nt * d + 4.0 * nt * ff) / hbm)
+                r = {"shape": shape, "grouped_experts": Gx, "n": n, "us": round(t * 1e6, 2),
+                     "tflops": round(flop / t / 1e12, 2), "weight_gbs": round(wbytes / t / 1e9, 1),
+                     "roofline_us": round(roof * 1e6, 2), "frac_of_roofline": round(roof / t, 3),
+                     "bound": "tensor" if flop / tc > wbytes / hbm else "hbm"}
+                print(json.dumps(r), flush=True)
+                results.append(r)
+                del gbs
+            ctx.close()
+            torch.cuda.empty_cache()
     if args.out:
         json.dump({"peaks": {"hbm_gbs": hbm / 1e9, "bf16_tflops": tc / 1e12}, "rows": results},
                   open(args.out, "w"), indent=1)
