@@ -220,6 +220,11 @@ template <> struct Vec<__nv_bfloat16> {
   }
   // value as stored (rounded), for sums over stored values
   __device__ __forceinline__ static float round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+  __device__ __forceinline__ static void unpack(const uint4& u, float* f) {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { float2 t = __bfloat1622float2(b[i]); f[2 * i] = t.x; f[2 * i + 1] = t.y; }
+  }
 };
 template <> struct Vec<float> {
   static constexpr int N = 4;
@@ -231,6 +236,9 @@ template <> struct Vec<float> {
     *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
   }
   __device__ __forceinline__ static float round(float v) { return v; }
+  __device__ __forceinline__ static void unpack(const uint4& u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y); f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
 };
 
 __device__ __forceinline__ float warp_sum(float v) {

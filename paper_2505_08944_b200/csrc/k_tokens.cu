@@ -257,7 +257,8 @@ __global__ void cdrain_kernel(DevCtx c) {
 
 // ---------------------------------------------------------------------------- combine (a8)
 
-template <typename T>
+// KSM: compile-time bound on K+S (2, 4, 8 or 12) sizing the per-chunk leg registers.
+template <typename T, int KSM>
 __global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int retire_pass) {
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
@@ -295,36 +296,29 @@ __global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int reti
       // together per leg so each lane keeps kU loads in flight.
       for (int k = c.K; k < c.KS; ++k) w[k] = 1.0f;
       float ss = 0.f;
-      for (int col0 = lane * V::N; col0 < c.d; col0 += kU * kWarp * V::N) {
-        float acc[kU][V::N];
+      for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
+        // all K+S legs of this 16-byte chunk are loaded before the (ordered) accumulation, so
+        // each lane keeps K+S+1 loads in flight (the leg count is a runtime value <= KSM)
+        uint4 raw[KSM];
+        const uint4 hraw = *reinterpret_cast<const uint4*>(h + col);
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int col = col0 + u * kWarp * V::N;
-          if (col < c.d) V::load(h + col, acc[u]);
-        }
-        for (int k = 0; k < c.KS; ++k) {
-          float o[kU][V::N];
-          const T* src = legrow + (uint64_t)k * c.d;
+        for (int k = 0; k < KSM; ++k)
+          if (k < c.KS) raw[k] = *reinterpret_cast<const uint4*>(legrow + (uint64_t)k * c.d + col);
+        float acc[V::N];
+        V::unpack(hraw, acc);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int col = col0 + u * kWarp * V::N;
-            if (col < c.d) V::load(src + col, o[u]);
-          }
-          const float wk = w[k];
+        for (int k = 0; k < KSM; ++k) {
+          if (k < c.KS) {
+            float o[V::N];
+            V::unpack(raw[k], o);
+            const float wk = w[k];
 #pragma unroll
-          for (int u = 0; u < kU; ++u)
-#pragma unroll
-            for (int j = 0; j < V::N; ++j) acc[u][j] = __fadd_rn(acc[u][j], __fmul_rn(wk, o[u][j]));
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int col = col0 + u * kWarp * V::N;
-          if (col < c.d) {
-            V::store(h + col, acc[u]);
-#pragma unroll
-            for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[u][j]); ss += r * r; }
+            for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(wk, o[j]));
           }
         }
+        V::store(h + col, acc);
+#pragma unroll
+        for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[j]); ss += r * r; }
       }
       ss = warp_sum(ss);
       rmsnorm_row<T>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);
@@ -390,8 +384,20 @@ int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
   // grid sized for the worst case (all homed tokens ready); idle CTAs exit at once
   int grid = (c.T + kTPC - 1) / kTPC;
   if (grid > 1184) grid = 1184;
-  if (c.dtype == AMOE_BF16) combine_kernel<__nv_bfloat16><<<grid, kTokThreads, 0, s>>>(c, retire_pass);
-  else combine_kernel<float><<<grid, kTokThreads, 0, s>>>(c, retire_pass);
+  const int ksm = c.KS <= 2 ? 2 : c.KS <= 4 ? 4 : c.KS <= 8 ? 8 : 12;
+#define AMOE_COMBINE(TT, KK) combine_kernel<TT, KK><<<grid, kTokThreads, 0, s>>>(c, retire_pass)
+  if (c.dtype == AMOE_BF16) {
+    if (ksm == 2) AMOE_COMBINE(__nv_bfloat16, 2);
+    else if (ksm == 4) AMOE_COMBINE(__nv_bfloat16, 4);
+    else if (ksm == 8) AMOE_COMBINE(__nv_bfloat16, 8);
+    else AMOE_COMBINE(__nv_bfloat16, 12);
+  } else {
+    if (ksm == 2) AMOE_COMBINE(float, 2);
+    else if (ksm == 4) AMOE_COMBINE(float, 4);
+    else if (ksm == 8) AMOE_COMBINE(float, 8);
+    else AMOE_COMBINE(float, 12);
+  }
+#undef AMOE_COMBINE
   return 2;
 }
 

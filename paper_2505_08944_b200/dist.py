@@ -33,18 +33,46 @@ def token_range(rank: int, T: int):
     return range(rank * T, rank * T + T)
 
 
-def peer_workspace(nbytes: int, device, group=None):
-    """Symmetric (peer-mapped) workspace: (tensor, [base address of every rank's buffer])."""
-    import torch.distributed._symmetric_memory as symm_mem
-    try:
-        symm_mem.set_backend("CUDA")
-    except Exception:
-        pass
-    ws = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
-    hdl = symm_mem.rendezvous(ws, group or dist.group.WORLD)
-    ptrs = [int(p) for p in hdl.buffer_ptrs]
+def peer_workspace(nbytes: int, device, group=None, method: str | None = None):
+    """Peer-mapped workspace: (tensor, [address of every rank's workspace, valid in THIS process]).
+
+    method "ipc" (default): each rank allocates its workspace with torch and publishes a CUDA IPC
+    handle through the process group (all_gather_object); every rank opens its peers' handles
+    (cudaIpcOpenMemHandle: NVLink peer mappings across GPUs, or same-device mappings when ranks
+    share a GPU). method "symm": torch symmetric memory (empty + rendezvous). Setup only."""
+    method = method or os.environ.get("AMOE_PEER_METHOD", "ipc")
+    if method == "symm":
+        import torch.distributed._symmetric_memory as symm_mem
+        try:
+            symm_mem.set_backend("CUDA")
+        except Exception:
+            pass
+        ws = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        hdl = symm_mem.rendezvous(ws, group or dist.group.WORLD)
+        ptrs = [int(p) for p in hdl.buffer_ptrs]
+        _keep = None
+    else:
+        from torch.multiprocessing.reductions import reduce_tensor
+        ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=device)
+        ws = ws[(-ws.data_ptr()) % 256:][:nbytes]
+        rebuild, rargs = reduce_tensor(ws)
+        world = dist.get_world_size(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, (rebuild, rargs), group=group)
+        me = dist.get_rank(group)
+        _keep = []
+        ptrs = []
+        for r, (fn, a) in enumerate(handles):
+            if r == me:
+                ptrs.append(ws.data_ptr())
+            else:
+                t = fn(*a)
+                _keep.append(t)
+                ptrs.append(t.data_ptr())
+        torch.cuda.synchronize()
     if any(p % 256 for p in ptrs):
-        raise RuntimeError("symmetric workspaces must be 256-byte aligned")
+        raise RuntimeError("peer workspaces must be 256-byte aligned")
+    peer_workspace._keep = getattr(peer_workspace, "_keep", []) + [_keep]
     return ws, ptrs
 
 
