@@ -242,6 +242,9 @@ def main():
         return ctx.run(retire_pass=p + 1, policy=policy, grouped=grouped)
 
     barrier = D.barrier
+    # every rank must have created (zeroed) its workspace before any rank pushes legs into it
+    torch.cuda.synchronize()
+    barrier()
 
     for w in range(args.warmup):
         step(w)

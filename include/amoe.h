@@ -142,8 +142,10 @@ size_t amoe_workspace_bytes(const amoe_config* cfg);
 amoe_status amoe_create(const amoe_config* cfg, void* workspace, size_t bytes, amoe_ctx_t* out);
 
 /* Register every rank's workspace base (host array [G] of device addresses valid in THIS
- * process: symm_mem.rendezvous(ws).buffer_ptrs, or local aliases for loopback tests).
- * peer_ws[rank] must equal this context's workspace. Setup only. */
+ * process: opened CUDA IPC handles / symm_mem buffer_ptrs, or local aliases for loopback tests).
+ * peer_ws[rank] must equal this context's workspace. Setup only. The caller must synchronise all
+ * ranks (device sync + process barrier) after every rank's amoe_create and before the first
+ * amoe_enqueue anywhere: amoe_create zeroes the rings that peers push legs into. */
 amoe_status amoe_import_peers(amoe_ctx_t ctx, const uint64_t* peer_ws, int G);
 
 /* Register expert weights of (layer, expert) hosted here (expert >= E: shared expert

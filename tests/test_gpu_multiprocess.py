@@ -43,6 +43,8 @@ def _rank_main(rank, world, port, T, q):
             for e in D.hosted_experts(P.E, P.S, world, rank):
                 ctx.set_expert(l, e, *P.Wd[(l, e)])
         ctx.set_router(torch.from_numpy(P.tables[rank]).cuda().contiguous())
+        torch.cuda.synchronize()
+        dist.barrier()           # all workspaces created (zeroed) before any rank pushes legs
         slots = torch.arange(T, dtype=torch.int32, device="cuda")
         ctx.token_init(slots, dev_tensor(P.h0[rank], "bf16"), 0)
         ctx.enqueue(0, slots, logits=torch.from_numpy(np.ascontiguousarray(P.tables[rank][0, 0])).cuda())
