@@ -52,6 +52,7 @@ struct FfnArgs {
   int32_t ring_legs;     // 1 = the drained legs are read from the µ-queue rings (no meta copy)
   int32_t gather;        // GATEUP: 1 = A rows gathered from x by token slot (TMA tile::gather4)
   int32_t allow_split;   // split K when the output tiles cannot fill the machine (cold experts)
+  int32_t atrim;         // partial M tiles load only their valid A rows
   float* part;           // split-K fp32 partials (workspace)
   uint32_t* cnt;         // split-K per-slot arrival counters (workspace, self-resetting)
   const amoe_leg* meta;  // [rows] drained legs (fused forward) when !ring_legs
@@ -453,7 +454,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
         // a partial M tile loads only its valid rows (32-row boxes); the rest of the smem tile
         // is stale and only feeds accumulator rows that are never stored
-        const int nA = (args.l2hint || rows_valid >= BM) ? 0 : (rows_valid + 31) / 32;
+        const int nA = (args.l2hint || !args.atrim || rows_valid >= BM) ? 0 : (rows_valid + 31) / 32;
         mbar_expect_tx(full, (nA ? nA * 32 * BK * 2 : A_BYTES) + BN * BK * 2);
         if (args.l2hint) {
           tma_load_2d_hint(sa, &tmA, kb * BK, arow, full, pol_a);
@@ -713,7 +714,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // partial M tile: each CTA loads only its valid rows in 32-row boxes (the leader's
         // expected byte count covers both CTAs' A rows and both B halves)
         const int rv0 = s_n[q] - m * BM2, rv1 = rv0 - 128;
-        auto a_loads = [&](int rv) { return (args.l2hint || rv >= 128) ? -1 : (rv <= 0 ? 0 : (rv + 31) / 32); };
+        auto a_loads = [&](int rv) {
+          return (args.l2hint || !args.atrim || rv >= 128) ? -1 : (rv <= 0 ? 0 : (rv + 31) / 32);
+        };
         auto a_bytes = [&](int rv) { const int l = a_loads(rv); return l < 0 ? HALF_BYTES : l * 32 * BK * 2; };
         if (leader) mbar_expect_tx(smem_u32(&bars[stage]), a_bytes(rv0) + a_bytes(rv1) + 2 * HALF_BYTES);
         const int nA = a_loads(crank ? rv1 : rv0);
@@ -933,6 +936,8 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.cnt = reinterpret_cast<uint32_t*>(c.peer[c.rank] + c.lay.split_cnt);
   const char* es = getenv("AMOE_SPLITK");
   a.allow_split = es ? (es[0] == '1') : 1;
+  const char* et = getenv("AMOE_ATRIM");
+  a.atrim = et ? (et[0] == '1') : 1;
   a.ring_legs = gathered;
   a.gather = (part == 1) ? gathered : 0;
   for (int q = 0; q < f.nq; ++q) a.wslot[q] = f.wslot[q];
