@@ -33,7 +33,6 @@ constexpr int GROUP_M = 16;
 // selects the 1-CTA kernel (UMMA M=128), which also serves d % 256 != 0
 constexpr bool kDefault1Cta = false;
 constexpr uint32_t kSuspendNs = 0x10000;   // mbarrier try_wait suspend-time hint (ns)
-constexpr bool kDefaultL2Hint = false;       // AMOE_L2HINT=1: TMA L2 eviction-priority hints
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;   // + barriers/tile tables + align
 
@@ -48,7 +47,6 @@ struct FfnArgs {
   int32_t w_which;       // 0 (W1; W3 = +1) or 2 (W2) within a queue's 3 tensor maps
   int32_t group_m;       // M tiles per raster group (L2 reuse of the weight slab)
   int32_t fuse;          // DOWN: 1 = store rows straight into the home token pools (fused a7)
-  int32_t l2hint;        // 1 = TMA loads carry L2 evict_last (tokens) / evict_first (weights)
   int32_t ring_legs;     // 1 = the drained legs are read from the µ-queue rings (no meta copy)
   int32_t gather;        // GATEUP: 1 = A rows gathered from x by token slot (TMA tile::gather4)
   int32_t allow_split;   // split K when the output tiles cannot fill the machine (cold experts)
@@ -92,26 +90,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar) : "memory");
-}
-// Same load with an L2 eviction-priority policy (createpolicy): token rows are re-read for every
-// N tile of their raster group (keep: evict_last); a weight slab is consumed by the group's
-// concurrently running M tiles and then dead until the next group (evict_first).
-__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const void* tmap, int c0, int c1, uint32_t bar,
-                                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;"
-      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar), "l"(policy) : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
 }
 // TMA tile::gather4: 4 rows (arbitrary row coordinates) x 64 columns into 4 consecutive 128-B
 // rows of a 128-B-swizzled tile (tensor map box {64, 1}; the swizzle follows the smem address,
@@ -422,22 +400,18 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     // ===================== TMA producer (lane 0; the whole warp when A rows are gathered:
     // lane i issues the tile::gather4 of tile rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
-    const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int t = u / split, ks = u - t * split;
       int q, m, nb;
       sc.decode(t, q, m, nb);
       const int arow = s_off[q] + m * BM;
-      const int rows_valid = s_n[q] - m * BM;
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
-      int4 rows4 = make_int4(0, 0, 0, 0);
-      if (MODE == MODE_GATEUP && args.gather) rows4 = gather_rows(args, dc, q, m * BM + lane * 4, s_n[q], s_start);
       const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const uint32_t full = smem_u32(&bars[stage]);
-        const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
-        const uint32_t sb = sa + A_BYTES;
-        if (MODE == MODE_GATEUP && args.gather) {
+      if (MODE == MODE_GATEUP && args.gather) {
+        const int4 rows4 = gather_rows(args, dc, q, m * BM + lane * 4, s_n[q], s_start);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const uint32_t full = smem_u32(&bars[stage]);
+          const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
           if (lane == 0) {
             mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
             mbar_expect_tx(full, A_BYTES + BN * BK * 2);
@@ -445,39 +419,50 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           __syncwarp();
           tma_gather4(sa + lane * 4 * 128, &tmA, kb * BK, rows4, full);
           if (lane == 0) {
-            tma_load_2d(sb, wb, kb * BK, nb * 128, full);
-            tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
+            tma_load_2d(sa + A_BYTES, wb, kb * BK, nb * 128, full);
+            tma_load_2d(sa + A_BYTES + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-          continue;
         }
-        mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
-        // a partial M tile loads only its valid rows (32-row boxes); the rest of the smem tile
-        // is stale and only feeds accumulator rows that are never stored
-        const int nA = (args.l2hint || !args.atrim || rows_valid >= BM) ? 0 : (rows_valid + 31) / 32;
-        mbar_expect_tx(full, (nA ? nA * 32 * BK * 2 : A_BYTES) + BN * BK * 2);
-        if (args.l2hint) {
-          tma_load_2d_hint(sa, &tmA, kb * BK, arow, full, pol_a);
-#pragma unroll
-          for (int h = 0; h < BN / 128; ++h) {
-            const CUtensorMap* m2 = (MODE == MODE_GATEUP) ? wb + h : wb;
-            const int r0 = (MODE == MODE_GATEUP) ? nb * 128 : nb * BN + h * 128;
-            tma_load_2d_hint(sb + h * 128 * BK * 2, m2, kb * BK, r0, full, pol_b);
-          }
+        continue;
+      }
+      // A partial M tile loads only its valid rows (32-row boxes); the rest of the smem tile is
+      // stale and only feeds accumulator rows that are never stored. Decided per tile, in its own
+      // loop: extra work between the empty-slot wait and the TMA issue delays every refill
+      // (measured: ~30% of the pair kernel's throughput).
+      const int rows_valid = s_n[q] - m * BM;
+      const int nA = (!args.atrim || rows_valid >= BM) ? 0 : (rows_valid + 31) / 32;
+      auto load_b = [&](uint32_t sb, int kb, uint32_t full) {
+        if (MODE == MODE_GATEUP) {
+          tma_load_2d(sb, wb, kb * BK, nb * 128, full);
+          tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
         } else {
-          if (nA == 0) tma_load_2d(sa, &tmA, kb * BK, arow, full);
-          else
-            for (int i = 0; i < nA; ++i) tma_load_2d(sa + i * 32 * BK * 2, &tmA32, kb * BK, arow + i * 32, full);
-          if (MODE == MODE_GATEUP) {
-            tma_load_2d(sb, wb, kb * BK, nb * 128, full);
-            tma_load_2d(sb + 128 * BK * 2, wb + 1, kb * BK, nb * 128, full);
-          } else {
-            // weight maps have 128-row boxes: BN = 256 takes two loads
+          // weight maps have 128-row boxes: BN = 256 takes two loads
 #pragma unroll
-            for (int h = 0; h < BN / 128; ++h) tma_load_2d(sb + h * 128 * BK * 2, wb, kb * BK, nb * BN + h * 128, full);
-          }
+          for (int h = 0; h < BN / 128; ++h) tma_load_2d(sb + h * 128 * BK * 2, wb, kb * BK, nb * BN + h * 128, full);
         }
-        if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+      };
+      if (nA == 0) {
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const uint32_t full = smem_u32(&bars[stage]);
+          const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
+          mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
+          mbar_expect_tx(full, A_BYTES + BN * BK * 2);
+          tma_load_2d(sa, &tmA, kb * BK, arow, full);
+          load_b(sa + A_BYTES, kb, full);
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        }
+      } else {
+        const uint32_t tx = nA * 32 * BK * 2 + BN * BK * 2;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const uint32_t full = smem_u32(&bars[stage]);
+          const uint32_t sa = smem_u32(tiles + stage * STAGE_BYTES);
+          mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1u);
+          mbar_expect_tx(full, tx);
+          for (int i = 0; i < nA; ++i) tma_load_2d(sa + i * 32 * BK * 2, &tmA32, kb * BK, arow + i * 32, full);
+          load_b(sa + A_BYTES, kb, full);
+          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -574,13 +559,6 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap,
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
 }
-__device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const void* tmap, int c0, int c1,
-                                                      uint32_t bar_cluster, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;"
-      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy) : "memory");
-}
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
@@ -624,8 +602,7 @@ struct Sched2 {
 
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
-ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA32, const FfnArgs args,
-               const __grid_constant__ DevCtx dc) {
+ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];
   __shared__ int s_last;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -683,7 +660,6 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
     // the leader's full barrier (whole warp when A rows are gathered: lane i -> rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
-    const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_first();
     for (int u = cl; u < units; u += ncl) {
       const int t = u / split, ks = u - t * split;
       const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
@@ -693,13 +669,11 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
       const CUtensorMap* bmap = (MODE == MODE_GATEUP) ? wb + crank : wb;
       const int brow = (MODE == MODE_GATEUP) ? nb * 128 : nb * 256 + (int)crank * 128;
-      int4 rows4 = make_int4(0, 0, 0, 0);
-      if (MODE == MODE_GATEUP && args.gather)
-        rows4 = gather_rows(args, dc, q, m * BM2 + (int)crank * 128 + lane * 4, s_n[q], s_start);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
-        const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
-        if (MODE == MODE_GATEUP && args.gather) {
+      if (MODE == MODE_GATEUP && args.gather) {
+        const int4 rows4 = gather_rows(args, dc, q, m * BM2 + (int)crank * 128 + lane * 4, s_n[q], s_start);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
+          const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
           if (lane == 0) {
             mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
             if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
@@ -708,28 +682,19 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           tma_gather4_pair(sa + lane * 4 * 128, &tmA, kb * BK, rows4, full_leader);
           if (lane == 0) tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
           if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
-          continue;
         }
+        continue;
+      }
+      // Full tiles only: trimming partial M tiles to their valid rows (as the 1-CTA producer
+      // does) measured ~15-25% slower here even when no tile was partial (the extra code between
+      // the empty-slot wait and the TMA issue; profiles/r01_pair_regression.md).
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
+        const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
         mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
-        // partial M tile: each CTA loads only its valid rows in 32-row boxes (the leader's
-        // expected byte count covers both CTAs' A rows and both B halves)
-        const int rv0 = s_n[q] - m * BM2, rv1 = rv0 - 128;
-        auto a_loads = [&](int rv) {
-          return (args.l2hint || !args.atrim || rv >= 128) ? -1 : (rv <= 0 ? 0 : (rv + 31) / 32);
-        };
-        auto a_bytes = [&](int rv) { const int l = a_loads(rv); return l < 0 ? HALF_BYTES : l * 32 * BK * 2; };
-        if (leader) mbar_expect_tx(smem_u32(&bars[stage]), a_bytes(rv0) + a_bytes(rv1) + 2 * HALF_BYTES);
-        const int nA = a_loads(crank ? rv1 : rv0);
-        if (args.l2hint) {
-          tma_load_2d_pair_hint(sa, &tmA, kb * BK, arow, full_leader, pol_a);
-          tma_load_2d_pair_hint(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader, pol_b);
-        } else {
-          if (nA < 0) tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
-          else
-            for (int i = 0; i < nA; ++i)
-              tma_load_2d_pair(sa + i * 32 * BK * 2, &tmA32, kb * BK, arow + i * 32, full_leader);
-          tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
-        }
+        if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
+        tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
+        tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
         if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
       }
     }
@@ -949,8 +914,6 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const char* eg = getenv("AMOE_GROUP_M");
   const int gm_rows = eg ? atoi(eg) : 2048;
   a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
-  const char* eh = getenv("AMOE_L2HINT");
-  a.l2hint = eh ? (eh[0] == '1') : kDefaultL2Hint;
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
     a.n_tiles = c.ff / 128;
@@ -981,10 +944,10 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     cfg.numAttrs = 1;
     const int slots = (num_sms & ~1) / 2;
     if (part == 1) {
-      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, tm_tile32, a, c);
+      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
       if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
     } else {
-      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, tm_act32, a, c);
+      cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
       if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
     }
     return a.allow_split ? 2 : 1;
