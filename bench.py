@@ -46,6 +46,13 @@ def parse():
     return ap.parse_args()
 
 
+def FFN_KERNEL(d):
+    """Name of the gate/up kernel the library launches (CTA pair unless d % 256 or AMOE_FFN_1CTA=1)."""
+    if d % 256 == 0 and os.environ.get("AMOE_FFN_1CTA", "0") != "1":
+        return "ffn_tc2_kernel<GATEUP> (tcgen05 cta_group::2 UMMA 256x256, fused SwiGLU)"
+    return "ffn_tc_kernel<GATEUP> (tcgen05 UMMA 128x256, fused SwiGLU)"
+
+
 def config_dict(spec, L, T, G, policy, grouped):
     """The workload description shared by both arms' JSON lines."""
     return {"workload": f"{spec.name}-shaped expert layers: L={L} E={spec.E} top-{spec.K} S={spec.S} d={spec.d} "
@@ -309,7 +316,7 @@ def main():
         "config": config_dict(spec, L, T, G, policy, grouped),
         "gpu_launches": int(launches),
         "clocks": clk,
-        "roofline": {"bound": "tensor", "kernel": "ffn_tc_kernel<GATEUP> (tcgen05, fused SwiGLU)",
+        "roofline": {"bound": "tensor", "kernel": FFN_KERNEL(d),
                      "achieved": gu_tflops, "peak": peak_sust, "unit": "TFLOP/s",
                      "frac": (gu_tflops / peak_sust) if gu_tflops else None,
                      "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",

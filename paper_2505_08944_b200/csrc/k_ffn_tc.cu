@@ -910,9 +910,11 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const char* ev = getenv("AMOE_FFN_1CTA");
   const bool force1 = ev ? ev[0] == '1' : kDefault1Cta;
   const bool pair = !force1 && c.d % 256 == 0 && num_sms >= 2;
-  // raster group: rows of a queue sharing a weight slab through L2 (tuning knob)
-  const char* eg = getenv("AMOE_GROUP_M");
-  const int gm_rows = eg ? atoi(eg) : 2048;
+  // raster group: rows of a queue sharing a weight slab through L2. 4096 rows: the lowest DRAM
+  // traffic measured (gate/up 11.5 GB vs 15.5 GB at 2048 on a Mixtral layer), which under the
+  // power cap buys SM clock (+4.5% FFN throughput; profiles/r01_group_m_sweep.md)
+  const char* eg = getenv(part == 2 && getenv("AMOE_GROUP_M_DOWN") ? "AMOE_GROUP_M_DOWN" : "AMOE_GROUP_M");
+  const int gm_rows = eg ? atoi(eg) : 4096;
   a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
