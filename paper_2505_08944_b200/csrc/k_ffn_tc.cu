@@ -34,7 +34,8 @@ constexpr int GROUP_M = 16;
 constexpr bool kDefault1Cta = false;
 constexpr uint32_t kSuspendNs = 0x10000;   // mbarrier try_wait suspend-time hint (ns)
 constexpr int TMEM_COLS = 512;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + 1024;   // + barriers/tile tables + align
+constexpr int EPI_STAGE_BYTES = 4 * 4096;       // epilogue store staging, 4 KB per epilogue warp
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4096 + EPI_STAGE_BYTES + 1024;   // + barriers/tables + align
 
 enum Mode { MODE_GATEUP = 0, MODE_DOWN = 1 };
 
@@ -155,6 +156,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // ------------------------------------------------------------------ tile schedule
 struct Sched {
   int nq, n_tiles, total, group;
@@ -233,46 +247,100 @@ __device__ __forceinline__ __nv_bfloat16* down_row_dst(const FfnArgs& a, const D
   return a.out + (uint64_t)grow * a.out_ld;
 }
 // ------------------------------------------------------------------ epilogue (shared by both kernels)
-// Final stores of one row of one unit from a value source src(col0, v[32]) — TMEM loads, or the
-// fixed-order sum of split-K partials. GATEUP: act = bf16(silu(g)·u); DOWN: out/pool = bf16(v)
-// (+ fused forward). src must be called by all 32 lanes (tcgen05.ld is warp-collective).
-template <int MODE, int BN, typename Src>
-__device__ __forceinline__ void store_row(const FfnArgs& args, const DevCtx& dc, Src src, bool valid,
-                                          __nv_bfloat16* orow, int nb, const amoe_leg& leg, unsigned long long* s_fwd) {
+// One row per thread leaves TMEM (tcgen05.ld 32x32b: lane = accumulator row). Stored directly,
+// every store instruction of a warp would touch 32 rows (32 half-filled sectors in 32 lines);
+// instead each 64-column chunk of the warp's 32 rows goes through a 4 KB smem stage (16-B
+// chunks XOR-swizzled by row: conflict-free both ways) and leaves as 4 whole 128-B row lines
+// per instruction.
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+// w: this lane's row (NW packed bf16x2 words = 2·NW columns starting at column col0 of the row
+// at dst; dst == nullptr: row not stored). ncols: valid columns of the row segment.
+template <int NW>
+__device__ __forceinline__ void store_rows_staged(const uint32_t (&w)[NW], __nv_bfloat16* dst, int col0, int ncols,
+                                                  uint32_t stage, int lane) {
+  static_assert(NW % 32 == 0, "64-column chunks");
+  const int c = lane & 7;
+  __nv_bfloat16* rdst[8];                 // destination rows 4 s + lane / 8 of this lane's stores
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    rdst[s] = reinterpret_cast<__nv_bfloat16*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), 4 * s + (lane >> 3)));
+#pragma unroll
+  for (int ch = 0; ch < NW / 32; ++ch) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      sts128(stage + lane * 128 + ((j ^ (lane & 7)) << 4), w[ch * 32 + 4 * j], w[ch * 32 + 4 * j + 1],
+             w[ch * 32 + 4 * j + 2], w[ch * 32 + 4 * j + 3]);
+    __syncwarp();
+    const int col = ch * 64 + c * 8;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int r = 4 * s + (lane >> 3);
+      const uint4 v = lds128(stage + r * 128 + ((c ^ (r & 7)) << 4));
+      if (rdst[s] && col < ncols) *reinterpret_cast<uint4*>(rdst[s] + col0 + col) = v;
+    }
+    __syncwarp();
+  }
+}
+
+// Non-split epilogue of one tile: every TMEM column this thread needs is loaded (and packed to
+// bf16) first, the accumulator is released to the MMA issuer, and only then do the global
+// stores (and, fused forward, the leg-piece counting) run — off the MMA's critical path.
+// GATEUP: act = bf16(silu(g)·u), 128 columns; DOWN: out / home pool = bf16(v), BN columns.
+template <int MODE, int BN, typename Release>
+__device__ __forceinline__ void epilogue_tile(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, bool valid,
+                                              __nv_bfloat16* orow, int nb, const amoe_leg& leg, uint32_t stage,
+                                              int lane, uint32_t (&fwd)[2], Release release) {
+  constexpr int NW = (MODE == MODE_GATEUP) ? 64 : BN / 2;
+  uint32_t w[NW];
   if (MODE == MODE_GATEUP) {
-#pragma unroll 1
-    for (int ch = 0; ch < 4; ++ch) {
-      float g[32], u[32];
-      src(ch * 32, g);
-      src(128 + ch * 32, u);
-      if (valid) {
-        uint4 pk[4];
-        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          p2[j] = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
-        uint4* dst = reinterpret_cast<uint4*>(orow + nb * 128 + ch * 32);
+    for (int ch = 0; ch < 8; ++ch) {
+      float g[16], u[16];
+      tmem_ld16(taddr + ch * 16, g);
+      tmem_ld16(taddr + 128 + ch * 16, u);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+      for (int j = 0; j < 8; ++j) {
+        __nv_bfloat162 p = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
+        w[ch * 8 + j] = *reinterpret_cast<uint32_t*>(&p);
       }
     }
   } else {
-#pragma unroll 1
-    for (int ch = 0; ch < BN / 32; ++ch) {
-      float v[32];
-      src(ch * 32, v);
-      const int col = nb * BN + ch * 32;
-      if (valid && col < args.out_cols) {
-        uint4 pk[4];
-        __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(pk);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) p2[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-        uint4* dst = reinterpret_cast<uint4*>(orow + col);
+    for (int ch = 0; ch < BN / 16; ++ch) {
+      float v[16];
+      tmem_ld16(taddr + ch * 16, v);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+      for (int j = 0; j < 8; ++j) {
+        __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        w[ch * 8 + j] = *reinterpret_cast<uint32_t*>(&p);
       }
     }
-    if (args.fuse && valid) down_row_done(args, dc, leg, nb, BN, s_fwd);
+  }
+  tc_fence_before();
+  release();                      // TMEM free: the MMA proceeds with the tile after next
+  __nv_bfloat16* dst = valid ? orow : nullptr;
+  if (MODE == MODE_GATEUP) {
+    store_rows_staged<NW>(w, dst, nb * 128, 128, stage, lane);
+  } else {
+    store_rows_staged<NW>(w, dst, nb * BN, min(BN, args.out_cols - nb * BN), stage, lane);
+    if (args.fuse) {
+      // every lane orders its own stores, then the row's owner lane counts the row's pieces
+      fence_sc(dc.G > 1);
+      __syncwarp();
+      const int cols = min(BN, dc.d - nb * BN);
+      if (valid && cols > 0) {
+        leg_pieces_done(dc, leg.home, leg.token_slot, leg.k, (uint32_t)(cols / 128));
+        if (nb == 0) { fwd[0] += 1; fwd[1] += (leg.home != dc.rank); }
+      }
+    }
   }
 }
 
@@ -283,13 +351,10 @@ __device__ __forceinline__ void store_row(const FfnArgs& args, const DevCtx& dc,
 template <int MODE, int BN, typename Release>
 __device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, int split, int ks,
                                               int slot, int rloc, bool valid, __nv_bfloat16* orow, int nb,
-                                              const amoe_leg& leg, unsigned long long* s_fwd, volatile int* s_last,
-                                              int tid, Release release) {
-  auto tmem_src = [&](int col0, float* v) { tmem_ld32(taddr + col0, v); };
+                                              const amoe_leg& leg, uint32_t stage, int lane, uint32_t (&fwd)[2],
+                                              Release release) {
   if (split <= 1) {
-    store_row<MODE, BN>(args, dc, tmem_src, valid, orow, nb, leg, s_fwd);
-    tc_fence_before();
-    release();
+    epilogue_tile<MODE, BN>(args, dc, taddr, valid, orow, nb, leg, stage, lane, fwd, release);
     return;
   }
   constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;      // fp32 columns per partial row
@@ -332,25 +397,11 @@ __device__ __forceinline__ int4 gather_rows(const FfnArgs& a, const DevCtx& dc, 
   for (int i = 0; i < 4; ++i) v[i] = (r0 + i < n) ? leg_of_row(a, dc, q, r0 + i, 0, s_start).token_slot : 0;
   return make_int4(v[0], v[1], v[2], v[3]);
 }
-// After this thread stored its row's columns of N tile nb: count the 128-column pieces
-// (release: the stores happen before), completing arrivals append to the combine ring.
-__device__ __forceinline__ void down_row_done(const FfnArgs& a, const DevCtx& dc, const amoe_leg& leg, int nb, int bn,
-                                              unsigned long long* s_fwd) {
-  const int cols = min(bn, dc.d - nb * bn);
-  if (cols <= 0) return;
-  leg_pieces_done(dc, leg.home, leg.token_slot, leg.k, (uint32_t)(cols / 128));
-  if (nb == 0) {
-    atomicAdd(&s_fwd[0], 1ull);
-    if (leg.home != dc.rank) atomicAdd(&s_fwd[1], 1ull);
-  }
-}
-
 template <int MODE, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA32, const FfnArgs args,
               const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];     // legs forwarded, of which remote
-  __shared__ int s_last;                      // split-K: this unit completes its tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -494,6 +545,8 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> registers -> global
     const int ew = warp - 4;            // TMEM lane quarter (warp % 4)
+    const uint32_t stage = smem_u32(smem + STAGES * STAGE_BYTES + 4096 + ew * 4096);
+    uint32_t fwd[2] = {0u, 0u};         // legs forwarded by this thread's rows, of which remote
     int acc = 0; uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int t = u / split, ks = u - t * split;
@@ -507,9 +560,17 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, s_off[q] + row, s_start, valid, leg);
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
       const uint32_t tempty = smem_u32(&bars[2 * STAGES + 2 + acc]);
-      epilogue_unit<MODE, BN>(args, dc, taddr, split, ks, t, ew * 32 + lane, valid, orow, nb, leg, s_fwd, &s_last, tid,
+      epilogue_unit<MODE, BN>(args, dc, taddr, split, ks, t, ew * 32 + lane, valid, orow, nb, leg, stage, lane, fwd,
                               [&] { epi_release_local(tempty, tid, 128); });
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+    if (MODE == MODE_DOWN && args.fuse) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        fwd[0] += __shfl_xor_sync(0xffffffffu, fwd[0], o);
+        fwd[1] += __shfl_xor_sync(0xffffffffu, fwd[1], o);
+      }
+      if (lane == 0) { atomicAdd(&s_fwd[0], (unsigned long long)fwd[0]); atomicAdd(&s_fwd[1], (unsigned long long)fwd[1]); }
     }
   }
   tc_fence_before();
@@ -537,7 +598,7 @@ using namespace tc;
 constexpr int STAGES2 = 6;
 constexpr int HALF_BYTES = 128 * BK * 2;                     // 16 KB
 constexpr int STAGE2_BYTES = 2 * HALF_BYTES;                 // A half + B half = 32 KB
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 4096 + 1024;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 4096 + EPI_STAGE_BYTES + 1024;
 constexpr int BM2 = 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -604,7 +665,6 @@ template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];
-  __shared__ int s_last;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -727,6 +787,8 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs): own 128 rows
     const int ew = warp - 4;
+    const uint32_t stage = smem_u32(smem + STAGES2 * STAGE2_BYTES + 4096 + ew * 4096);
+    uint32_t fwd[2] = {0u, 0u};
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&bars[2 * STAGES2 + 2]), 0);
     for (int u = cl; u < units; u += ncl) {
@@ -743,12 +805,20 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       const uint32_t tempty = tempty_leader0 + (uint32_t)(acc * 8);
       // each CTA's half tile is its own split-K slot: 2 t + crank
       epilogue_unit<MODE, 256>(args, dc, taddr, split, ks, 2 * t + (int)crank, ew * 32 + lane, valid, orow, nb, leg,
-                               s_fwd, &s_last, tid, [&] {
+                               stage, lane, fwd, [&] {
                                  __syncwarp();
                                  asm volatile("bar.sync 1, 128;" ::: "memory");
                                  if (tid == 128) mbar_arrive_cluster(tempty);
                                });
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+    }
+    if (MODE == MODE_DOWN && args.fuse) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        fwd[0] += __shfl_xor_sync(0xffffffffu, fwd[0], o);
+        fwd[1] += __shfl_xor_sync(0xffffffffu, fwd[1], o);
+      }
+      if (lane == 0) { atomicAdd(&s_fwd[0], (unsigned long long)fwd[0]); atomicAdd(&s_fwd[1], (unsigned long long)fwd[1]); }
     }
   }
   tc_fence_before();
