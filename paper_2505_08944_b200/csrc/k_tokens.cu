@@ -25,39 +25,46 @@ struct PendingLeg {
 
 // ---------------------------------------------------------------------------- routing (a1)
 // Warp-cooperative top-K of z[0..E) (ties -> lower expert index) and softmax over the K
-// selected logits; every lane returns the same idx/w. fp32 expf (oracle: float64, |Δw| ≤ 1e-6).
-__device__ __forceinline__ void route_warp(const float* __restrict__ z, int E, int K, int lane,
-                                           int* idx, float* w) {
-  float v[AMOE_MAX_E / kWarp];
-  uint32_t chosen = 0;
+// selected logits. Split in two so callers can issue the logit loads early: route_load reads
+// lane's share of z (expert lane + 32 j), route_select returns, in lane k < K, the k-th expert
+// and its weight (other lanes: -1, 0). fp32 expf, denominator summed in k order (oracle: float64,
+// |Δw| ≤ 1e-6). Everything stays in registers (K is a runtime value <= kMaxKS).
+constexpr int kZJ = AMOE_MAX_E / kWarp;
+__device__ __forceinline__ void route_load(const float* __restrict__ z, int E, int lane, float (&v)[kZJ]) {
 #pragma unroll
-  for (int j = 0; j < AMOE_MAX_E / kWarp; ++j) {
-    int e = lane + kWarp * j;
+  for (int j = 0; j < kZJ; ++j) {
+    const int e = lane + kWarp * j;
     v[j] = e < E ? z[e] : -INFINITY;
   }
-  float zs[kMaxKS];
+}
+__device__ __forceinline__ void route_select(const float (&v)[kZJ], int E, int K, int lane, int& my_e, float& my_w) {
+  uint32_t chosen = 0;
+  float my_z = 0.f, z0 = 0.f;
+  my_e = -1;
+#pragma unroll 1
   for (int k = 0; k < K; ++k) {
     float bv = -INFINITY;
     int be = 0x7fffffff;
 #pragma unroll
-    for (int j = 0; j < AMOE_MAX_E / kWarp; ++j) {
-      int e = lane + kWarp * j;
+    for (int j = 0; j < kZJ; ++j) {
+      const int e = lane + kWarp * j;
       if (e < E && !((chosen >> j) & 1u) && (v[j] > bv || be == 0x7fffffff)) { bv = v[j]; be = e; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
       if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
     }
-    idx[k] = be;
-    zs[k] = bv;
+    if (k == 0) z0 = bv;
+    if (lane == k) { my_e = be; my_z = bv; }
     if ((be & (kWarp - 1)) == lane) chosen |= 1u << (be / kWarp);
   }
-  float s = 0.f;
-  float ex[kMaxKS];
-  for (int k = 0; k < K; ++k) { ex[k] = expf(zs[k] - zs[0]); s += ex[k]; }
-  for (int k = 0; k < K; ++k) w[k] = ex[k] / s;
+  const float ex = lane < K ? expf(my_z - z0) : 0.f;
+  float sum = 0.f;
+#pragma unroll 1
+  for (int k = 0; k < K; ++k) sum += __shfl_sync(0xffffffffu, ex, k);
+  my_w = lane < K ? ex / sum : 0.f;
 }
 
 // ---------------------------------------------------------------------------- scatter (a2)
@@ -101,19 +108,18 @@ __device__ void scatter_legs(const DevCtx& c, const PendingLeg* legs, int n) {
 }
 
 // Fill the K (+S) legs of one routed token (lanes < K+S write their own leg).
-__device__ __forceinline__ void make_legs(const DevCtx& c, int layer, int slot, const int* idx,
-                                          const float* w, int lane, PendingLeg* out) {
+__device__ __forceinline__ void make_legs(const DevCtx& c, int layer, int slot, int my_e, float my_w, int lane,
+                                          PendingLeg* out) {
   if (lane < c.K) {
-    const int e = idx[lane];
     PendingLeg p;
-    if (e < 0 || e >= c.E) {
-      raise_fault(c, F_EXPERT_RANGE, slot, e, layer);
+    if (my_e < 0 || my_e >= c.E) {
+      raise_fault(c, F_EXPERT_RANGE, slot, my_e, layer);
       p.r = -1;
     } else {
-      p.r = c.owner[e];
-      p.q = layer * c.H + c.lq[e];
+      p.r = c.owner[my_e];
+      p.q = layer * c.H + c.lq[my_e];
     }
-    p.g.token_slot = slot; p.g.k = (int16_t)lane; p.g.home = (int16_t)c.rank; p.g.w = w[lane]; p.g.seq = 0;
+    p.g.token_slot = slot; p.g.k = (int16_t)lane; p.g.home = (int16_t)c.rank; p.g.w = my_w; p.g.seq = 0;
     out[lane] = p;
   } else if (lane < c.KS) {
     PendingLeg p;
@@ -199,22 +205,25 @@ __global__ void __launch_bounds__(kTokThreads) enqueue_kernel(DevCtx c, int laye
       if (i >= n) continue;
       const int slot = slots[i];
       if (slot < 0 || slot >= c.T) { if (lane == 0) raise_fault(c, F_SLOT_RANGE, slot, c.T, 1); continue; }
-      int idx[kMaxKS];
-      float w[kMaxKS];
+      int my_e = -1;
+      float my_w = 0.f;
       if (logits) {
-        route_warp(logits + (uint64_t)i * c.E, c.E, c.K, lane, idx, w);
-      } else {
-        for (int k = 0; k < c.K; ++k) { idx[k] = tidx[(uint64_t)i * c.K + k]; w[k] = tw[(uint64_t)i * c.K + k]; }
+        float zv[kZJ];
+        route_load(logits + (uint64_t)i * c.E, c.E, lane, zv);
+        route_select(zv, c.E, c.K, lane, my_e, my_w);
+      } else if (lane < c.K) {
+        my_e = tidx[(uint64_t)i * c.K + lane];
+        my_w = tw[(uint64_t)i * c.K + lane];
       }
       if (lane < c.K) {
-        wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = idx[lane];
-        wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = w[lane];
+        wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = my_e;
+        wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = my_w;
       }
       if (lane == 0) {
         wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
         wsp<int32_t>(c, c.rank, c.lay.tok_layer)[slot] = layer;
       }
-      make_legs(c, layer, slot, idx, w, lane, my);
+      make_legs(c, layer, slot, my_e, my_w, lane, my);
     }
     __syncthreads();
     scatter_legs(c, legs, kTPC * c.KS);
@@ -259,7 +268,7 @@ __global__ void cdrain_kernel(DevCtx c) {
 
 // KSM: compile-time bound on K+S (2, 4, 8 or 12) sizing the per-chunk leg registers.
 template <typename T, int KSM>
-__global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int retire_pass) {
+__global__ void __launch_bounds__(kTokThreads, (KSM <= 4 ? 4 : 2)) combine_kernel(DevCtx c, int retire_pass) {
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   __shared__ unsigned long long s_merged, s_retired;
@@ -287,14 +296,22 @@ __global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int reti
       const amoe_leg e = ring[pos & c.cring_mask];
       if (e.seq != pos + 1u) { if (lane == 0) raise_fault(c, F_STALE_ENTRY, 0xffffffffu, pos, e.seq); continue; }
       const int slot = e.token_slot;
-      float w[kMaxKS];
-      for (int k = 0; k < c.K; ++k) w[k] = tokw[(uint64_t)slot * c.K + k];
+      // the token's next position (layer + 1, or layer 0 of the next pass) and, unless it
+      // retires, its router logits there: loaded before the merge so their latency overlaps it
+      int layer = tlayer[slot] + 1;
+      int pass = tpass[slot];
+      if (layer == c.L) { layer = 0; ++pass; }
+      const bool retire = pass >= retire_pass;
+      float zv[kZJ];
+      if (!retire && c.router)
+        route_load(c.router + (((uint64_t)(pass % c.n_tab) * c.L + layer) * c.T + slot) * c.E, c.E, lane, zv);
+      // h_new = store(h + Σ_k w_k O_k + Σ_j O_shared_j), ascending k then j, no FMA (c9);
+      // shared legs use w = 1 (1·O == O exactly)
+      float w[KSM];
+#pragma unroll
+      for (int k = 0; k < KSM; ++k) w[k] = k < c.K ? tokw[(uint64_t)slot * c.K + k] : 1.0f;
       T* h = hbase + (uint64_t)slot * c.d;
       const T* legrow = pool + (uint64_t)slot * c.KS * c.d;
-      // h_new = store(h + Σ_k w_k O_k + Σ_j O_shared_j), ascending k then j, no FMA (c9);
-      // shared legs use w = 1 (1·O == O exactly). kU 16-byte chunks per lane are loaded
-      // together per leg so each lane keeps kU loads in flight.
-      for (int k = c.K; k < c.KS; ++k) w[k] = 1.0f;
       float ss = 0.f;
       for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
         // all K+S legs of this 16-byte chunk are loaded before the (ordered) accumulation, so
@@ -322,25 +339,21 @@ __global__ void __launch_bounds__(kTokThreads) combine_kernel(DevCtx c, int reti
       }
       ss = warp_sum(ss);
       rmsnorm_row<T>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);
-      int layer = tlayer[slot] + 1;
-      int pass = tpass[slot];
-      if (layer == c.L) { layer = 0; ++pass; }
       if (lane == 0) { tlayer[slot] = layer; tpass[slot] = pass; atomicAdd(&s_merged, 1ull); }
-      if (pass >= retire_pass) {
+      if (retire) {
         if (lane == 0) atomicAdd(&s_retired, 1ull);
         continue;
       }
       if (!c.router) { if (lane == 0) raise_fault(c, F_NO_ROUTER, slot, layer, pass); continue; }
-      int idx[kMaxKS];
-      float wn[kMaxKS];
-      const float* z = c.router + (((uint64_t)(pass % c.n_tab) * c.L + layer) * c.T + slot) * c.E;
-      route_warp(z, c.E, c.K, lane, idx, wn);
+      int my_e;
+      float my_w;
+      route_select(zv, c.E, c.K, lane, my_e, my_w);
       if (lane < c.K) {
-        wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = idx[lane];
-        wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = wn[lane];
+        wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = my_e;
+        wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = my_w;
       }
       if (lane == 0) wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
-      make_legs(c, layer, slot, idx, wn, lane, my);
+      make_legs(c, layer, slot, my_e, my_w, lane, my);
     }
     __syncthreads();
     scatter_legs(c, legs, kTPC * c.KS);
@@ -381,10 +394,31 @@ int launch_enqueue(const DevCtx& c, int layer, const int32_t* slots, int n, cons
 
 int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
   cdrain_kernel<<<1, 32, 0, s>>>(c);
-  // grid sized for the worst case (all homed tokens ready); idle CTAs exit at once
-  int grid = (c.T + kTPC - 1) / kTPC;
-  if (grid > 1184) grid = 1184;
+  // persistent grid: every resident CTA slot once (no tail wave), capped by the worst case (all
+  // homed tokens ready); CTAs loop over 32-token chunks of the ready list
   const int ksm = c.KS <= 2 ? 2 : c.KS <= 4 ? 4 : c.KS <= 8 ? 8 : 12;
+  static int resident[2][4] = {{0}};
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int& occ = resident[c.dtype == AMOE_BF16 ? 0 : 1][ksm == 2 ? 0 : ksm == 4 ? 1 : ksm == 8 ? 2 : 3];
+#define AMOE_OCC(TT, KK) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, combine_kernel<TT, KK>, kTokThreads, 0)
+  if (!occ) {
+    if (c.dtype == AMOE_BF16) {
+      if (ksm == 2) AMOE_OCC(__nv_bfloat16, 2); else if (ksm == 4) AMOE_OCC(__nv_bfloat16, 4);
+      else if (ksm == 8) AMOE_OCC(__nv_bfloat16, 8); else AMOE_OCC(__nv_bfloat16, 12);
+    } else {
+      if (ksm == 2) AMOE_OCC(float, 2); else if (ksm == 4) AMOE_OCC(float, 4);
+      else if (ksm == 8) AMOE_OCC(float, 8); else AMOE_OCC(float, 12);
+    }
+    if (occ < 1) occ = 1;
+  }
+#undef AMOE_OCC
+  int grid = (c.T + kTPC - 1) / kTPC;
+  if (grid > sms * occ) grid = sms * occ;
 #define AMOE_COMBINE(TT, KK) combine_kernel<TT, KK><<<grid, kTokThreads, 0, s>>>(c, retire_pass)
   if (c.dtype == AMOE_BF16) {
     if (ksm == 2) AMOE_COMBINE(__nv_bfloat16, 2);
