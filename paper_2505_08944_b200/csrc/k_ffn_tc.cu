@@ -746,8 +746,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
         continue;
       }
       // Full tiles only: trimming partial M tiles to their valid rows (as the 1-CTA producer
-      // does) measured ~15-25% slower here even when no tile was partial (the extra code between
-      // the empty-slot wait and the TMA issue; profiles/r01_pair_regression.md).
+      // does) measured ~15-25% slower here even when no tile was partial, and an out-of-line
+      // trimmed loop for the cold (split-K) units gained nothing measurable
+      // (profiles/r01_pair_regression.md).
       for (int kb = kb0; kb < kb1; ++kb) {
         const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
         const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
@@ -850,6 +851,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
   constexpr int CPL = (MODE == MODE_GATEUP ? 128 : BN) / 32;  // output columns per lane
   __shared__ int s_n[AMOE_MAX_GROUP], s_off[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP], s_pre[AMOE_MAX_GROUP + 1];
   __shared__ int s_mmax;
+  __shared__ int s_rpre[AMOE_MAX_GROUP + 1];   // prefix of valid (tile, row) items per queue
   const int nq = args.nq;
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
     s_n[q] = args.qinfo[q]; s_off[q] = args.qinfo[AMOE_MAX_GROUP + q]; s_start[q] = args.qinfo[2 * AMOE_MAX_GROUP + q];
@@ -863,6 +865,9 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
     }
     s_pre[nq] = acc;
     s_mmax = mm;
+    int ri = 0;
+    for (int q = 0; q < nq; ++q) { s_rpre[q] = ri; ri += s_n[q] * args.n_tiles; }
+    s_rpre[nq] = ri;
   }
   __syncthreads();
   const int total = s_pre[nq];
@@ -870,14 +875,17 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
   if (split <= 1) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  const int items = total * HALVES * 128;
+  // a split launch has every queue in one M tile (m = 0), so tile t = pre[q] + nb: only the
+  // valid rows (q, nb, row < n_q) are visited
+  const int items = s_rpre[nq];
   for (int it = gw; it < items; it += nw) {
-    const int t = it / (HALVES * 128), rem = it - t * HALVES * 128, h = rem / 128, r = rem - h * 128;
-    int q, m, nb;
-    if (PAIR) tc2::Sched2{nq, args.n_tiles, total, args.group_m, s_n, s_pre}.decode(t, q, m, nb);
-    else Sched{nq, args.n_tiles, total, args.group_m, s_n, s_off, s_pre}.decode(t, q, m, nb);
-    const int row = m * BMx + h * 128 + r;
-    if (row >= s_n[q]) continue;
+    int lo = 0, hi = nq - 1;
+    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (s_rpre[mid] <= it) lo = mid; else hi = mid - 1; }
+    const int q = lo;
+    const int r0 = it - s_rpre[q];
+    const int nb = r0 / s_n[q], row = r0 - nb * s_n[q];
+    const int t = s_pre[q] + nb;
+    const int h = row / 128, r = row - h * 128;
     const int slot = PAIR ? 2 * t + h : t;
     const float* base = args.part + ((size_t)slot * split * 128 + r) * W;
     const int grow = s_off[q] + row;
@@ -886,12 +894,22 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
       float g[CPL], u[CPL];
 #pragma unroll
       for (int j = 0; j < CPL; ++j) { g[j] = 0.f; u[j] = 0.f; }
-      for (int s = 0; s < split; ++s) {
-        const float* p = base + (size_t)s * 128 * W;
-        const float4 a = *reinterpret_cast<const float4*>(p + c);
-        const float4 b = *reinterpret_cast<const float4*>(p + 128 + c);
-        g[0] += a.x; g[1] += a.y; g[2] += a.z; g[3] += a.w;
-        u[0] += b.x; u[1] += b.y; u[2] += b.z; u[3] += b.w;
+      // partials summed in ks order; loads issued 4 splits at a time (latency, not bandwidth)
+      for (int s0 = 0; s0 < split; s0 += 4) {
+        float4 a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (s0 + i < split) {
+            const float* p = base + (size_t)(s0 + i) * 128 * W;
+            a[i] = *reinterpret_cast<const float4*>(p + c);
+            b[i] = *reinterpret_cast<const float4*>(p + 128 + c);
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (s0 + i < split) {
+            g[0] += a[i].x; g[1] += a[i].y; g[2] += a[i].z; g[3] += a[i].w;
+            u[0] += b[i].x; u[1] += b[i].y; u[2] += b[i].z; u[3] += b[i].w;
+          }
       }
       __nv_bfloat162 o[2];
       o[0] = __floats2bfloat162_rn(silu_mul(g[0], u[0]), silu_mul(g[1], u[1]));
@@ -902,13 +920,23 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
       float v[CPL];
 #pragma unroll
       for (int j = 0; j < CPL; ++j) v[j] = 0.f;
-      for (int s = 0; s < split; ++s) {
-        const float* p = base + (size_t)s * 128 * W + c;
+      for (int s0 = 0; s0 < split; s0 += 4) {
+        float4 a[4][CPL / 4];
 #pragma unroll
-        for (int j = 0; j < CPL; j += 4) {
-          const float4 a = *reinterpret_cast<const float4*>(p + j);
-          v[j] += a.x; v[j + 1] += a.y; v[j + 2] += a.z; v[j + 3] += a.w;
-        }
+        for (int i = 0; i < 4; ++i)
+          if (s0 + i < split) {
+            const float* p = base + (size_t)(s0 + i) * 128 * W + c;
+#pragma unroll
+            for (int j = 0; j < CPL / 4; ++j) a[i][j] = *reinterpret_cast<const float4*>(p + 4 * j);
+          }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (s0 + i < split) {
+#pragma unroll
+            for (int j = 0; j < CPL / 4; ++j) {
+              v[4 * j] += a[i][j].x; v[4 * j + 1] += a[i][j].y; v[4 * j + 2] += a[i][j].z; v[4 * j + 3] += a[i][j].w;
+            }
+          }
       }
       amoe_leg leg;
       __nv_bfloat16* orow = down_row_dst<MODE>(args, dc, q, row, grow, s_start, true, leg);
@@ -923,9 +951,9 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
         }
       }
       if (args.fuse) {
+        fence_sc(dc.G > 1);            // every lane's row stores before the piece count
         __syncwarp();
         if (lane == 0) {
-          fence_sc(dc.G > 1);          // the warp's row stores before the piece count
           const int cols = min(BN, dc.d - nb * BN);
           if (cols > 0) leg_pieces_done(dc, leg.home, leg.token_slot, leg.k, (uint32_t)(cols / 128));
           if (nb == 0) {

@@ -27,12 +27,16 @@ def main():
     ap.add_argument("--shapes", default="mixtral,deepseek")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--ns", default="", help="comma-separated subset of n values")
     ap.add_argument("--grouped", type=int, default=0,
                     help="also measure G distinct experts with n tokens each in ONE grouped launch "
                          "(what the Algorithm-1 grouped pick executes for cold layers)")
     args = ap.parse_args()
     import torch
     from paper_2505_08944_b200 import amoe
+    global NS
+    if args.ns:
+        NS = sorted(int(x) for x in args.ns.split(","))
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0) * 1e9
