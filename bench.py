@@ -36,13 +36,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=["mixtral", "deepseek", "tiny"])
-    ap.add_argument("--policy", default="defrag", choices=["defrag", "mtfs", "flfs"])
+    ap.add_argument("--policy", default="defrag", choices=["defrag", "mtfs", "flfs", "sync"],
+                    help="sync = synchronous-EP baseline: lockstep layers, box-wide barrier per layer")
     ap.add_argument("--ungrouped", action="store_true", help="one (layer, expert) queue per launch")
     ap.add_argument("--T", type=int, default=0, help="override tokens in flight per GPU")
     ap.add_argument("--L", type=int, default=0, help="override layers (parity/debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--skew", default="zipf", choices=["zipf", "exp"],
+                    help="routing skew: Zipf s=1.2 (BASELINE.json) or the paper's exponential fit (λ=0.38)")
     return ap.parse_args()
 
 
@@ -53,13 +56,44 @@ def FFN_KERNEL(d):
     return "ffn_tc_kernel<GATEUP> (tcgen05 UMMA 128x256, fused SwiGLU)"
 
 
-def config_dict(spec, L, T, G, policy, grouped):
+def config_dict(spec, L, T, G, policy, grouped, skew="zipf"):
     """The workload description shared by both arms' JSON lines."""
     return {"workload": f"{spec.name}-shaped expert layers: L={L} E={spec.E} top-{spec.K} S={spec.S} d={spec.d} "
-                        f"ff={spec.ff}, {T} tokens in flight per GPU, Zipf s={spec.zipf_s} routing",
+                        f"ff={spec.ff}, {T} tokens in flight per GPU, "
+                        + (f"Zipf s={spec.zipf_s}" if skew == "zipf" else "exponential λ=0.38") + " routing",
             "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped,
             "l2": "inputs larger than L2 (resident weights >> 126 MB); no flush",
             "step": "one decode pass: every token through all L layers"}
+
+
+def peaks_bf16():
+    """(burst, sustained, label): the driver-measured bf16 peaks, else the profiling guide's
+    fallback (1.59 PFLOP/s burst, ~1.4 sustained under the power cap), labelled as such."""
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return (float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]),
+                "of measured: sustained bf16 cuBLAS (MEASURED_PEAKS.json)")
+    except Exception:
+        return 1590.0, 1400.0, "of fallback: 1.4 PFLOP/s sustained bf16 (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def peak_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "of measured"
+    except Exception:
+        return 6650.0, "of fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config, kernel, L, T):
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` summary,
+    used only when the capture is of this kernel and workload (else null)."""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get(config, {})
+    except Exception:
+        return None
+    if rec.get("kernel") != kernel.split(" ")[0] or rec.get("T") != T:
+        return None
+    return rec.get("ffn_gateup_dram_bytes_per_launch")
 
 
 def dist_env():
@@ -233,7 +267,8 @@ def main():
             ctx.set_expert(l, e, w1, w3, w2)
             wts.append((w1, w3, w2))
     n_tab = 2
-    tables_host = [wl.router_logits(args.seed, L, T, E, zipf_s=spec.zipf_s, pass_idx=p, token_offset=rank * T)
+    tables_host = [wl.router_logits(args.seed, L, T, E, zipf_s=spec.zipf_s, pass_idx=p, token_offset=rank * T,
+                                    skew=args.skew)
                    for p in range(n_tab)]
     table = torch.from_numpy(np.stack(tables_host)).to(dev).contiguous()
     ctx.set_router(table)
@@ -282,51 +317,58 @@ def main():
     ctx.check()
     token_layers = sum(r["token_layers"] for r in runs)
     legs = sum(r["legs"] for r in runs)
+    # per-GPU stall: host wall time of scheduler polls that found nothing of this rank's to run
+    stall = D.gather_values([sum(r["idle_ns"] for r in runs) / max(1, sum(r["wall_ns"] for r in runs)),
+                             sum(r["barriers"] for r in runs)], device=dev)
     ms, (token_layers, legs) = D.reduce_timing(ms, [token_layers, legs], device=dev)
     assert token_layers == G * T * L * args.steps, (token_layers, G * T * L * args.steps)
     value = token_layers / (ms / 1e3)
 
     # roofline of the dominant kernel (tcgen05 gate/up + SwiGLU GEMM): algorithmic FLOPs per
     # launch = 4 d ff n (n = legs in the launch) over its CUDA-event duration
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak_burst = peaks.get("bf16_tflops", 1590.0)
-    peak_sust = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_burst, peak_sust, peak_kind = peaks_bf16()
     my_legs = sum(r["legs"] for r in runs)
     gu_ms, gu_n = prof["ffn_gateup"]
     dn_ms, dn_n = prof["ffn_down"]
     gu_tflops = 4.0 * d * ff * my_legs / (gu_ms / 1e3) / 1e12 if gu_ms else None
     dn_tflops = 2.0 * d * ff * my_legs / (dn_ms / 1e3) / 1e12 if dn_ms else None
-    traffic = None
-    try:
-        prof_sum = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = prof_sum.get(args.config, {}).get("ffn_gateup_dram_bytes_per_launch")
-    except Exception:
-        pass
+    traffic = ncu_traffic(args.config, FFN_KERNEL(d), L, T)
     stage_ms = {k: round(v[0], 3) for k, v in prof.items()}
+    # HBM-bound steps (SURVEY.md §8(d) per-unit bytes): combine+RMSNorm+route/scatter per
+    # token-layer = (K+S)·d·2 pool + 3·d·2 (h in, h out, x out) + E·4 logits; re-batch per leg =
+    # 2·d·2 (x row in, tile row out)
+    hbm_pk, hbm_kind = peak_hbm()
+    my_tl = sum(r["token_layers"] for r in runs)
+    hbm = {}
+    for name, nbytes, ms_ in (("combine", my_tl * ((K + S) * d * 2 + 3 * d * 2 + E * 4), prof["combine"][0]),
+                              ("rebatch", my_legs * 4 * d, prof["rebatch"][0])):
+        if ms_:
+            gbs = nbytes / (ms_ / 1e3) / 1e9
+            hbm[name] = {"achieved": round(gbs, 1), "peak": hbm_pk, "unit": "GB/s", "frac": round(gbs / hbm_pk, 3),
+                         "peak_kind": hbm_kind, "algorithmic_bytes": int(nbytes)}
     step_ms = ms / args.steps
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
-        "config": config_dict(spec, L, T, G, policy, grouped),
+        "config": config_dict(spec, L, T, G, policy, grouped, args.skew),
         "gpu_launches": int(launches),
         "clocks": clk,
+        "stall": {"idle_frac_per_rank": [round(v[0], 4) for v in stall], "layer_barriers": int(stall[0][1]),
+                  "definition": "time a rank's scheduler found no runnable queue / its amoe_run wall time"},
         "roofline": {"bound": "tensor", "kernel": FFN_KERNEL(d),
                      "achieved": gu_tflops, "peak": peak_sust, "unit": "TFLOP/s",
                      "frac": (gu_tflops / peak_sust) if gu_tflops else None,
-                     "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
+                     "peak_kind": peak_kind,
                      "frac_of_burst": (gu_tflops / peak_burst) if gu_tflops else None,
                      "traffic": traffic,
                      "algorithmic": "4*d*ff FLOP per leg (gate+up), legs per launch = drained tokens",
                      "down_kernel_tflops": dn_tflops,
                      "ffn_tflops": (6.0 * d * ff * my_legs / ((gu_ms + dn_ms) / 1e3) / 1e12) if gu_ms else None,
                      "stage_ms_total": stage_ms,
-                     "stage_launches": {k: v[1] for k, v in prof.items()}},
+                     "stage_launches": {k: v[1] for k, v in prof.items()},
+                     "hbm_kernels": hbm},
     }
 
     # ------------------------------------------------------------------ end to end (host buffers)

@@ -68,7 +68,12 @@ typedef struct amoe_ctx amoe_ctx;
 typedef amoe_ctx* amoe_ctx_t;
 
 typedef enum amoe_dtype { AMOE_BF16 = 0, AMOE_FP32 = 1 } amoe_dtype;
-typedef enum amoe_policy { AMOE_DEFRAG = 0, AMOE_MTFS = 1, AMOE_FLFS = 2 } amoe_policy;
+/* AMOE_SYNC is the synchronous expert-parallel baseline on the same kernels (SURVEY.md §8(f) f1,
+ * PAPER.md L65-L66, L123): layers run in lockstep; a rank takes layer l+1 only after every rank's
+ * homed tokens have merged layer l (a box-wide barrier per layer, flags stored into every peer's
+ * workspace), which is the dependency an all-to-all before and after each expert layer imposes.
+ * Every admitted token must start at the layer of this rank's last amoe_enqueue call. */
+typedef enum amoe_policy { AMOE_DEFRAG = 0, AMOE_MTFS = 1, AMOE_FLFS = 2, AMOE_SYNC = 3 } amoe_policy;
 
 /* Model / placement configuration. */
 typedef struct amoe_config {
@@ -129,6 +134,10 @@ typedef struct amoe_run_stats {
   int64_t token_layers;    /* merges completed on this rank (homed tokens) */
   int64_t kernel_launches; /* libamoe kernels launched */
   int64_t idle_polls;      /* scheduler polls that found nothing to run */
+  int64_t idle_ns;         /* host wall time of those polls: the GPU had nothing of this rank's
+                              queues to run (each poll synchronises the stream first) = stall */
+  int64_t wall_ns;         /* host wall time of the whole amoe_run call */
+  int64_t barriers;        /* AMOE_SYNC: layer barriers passed */
 } amoe_run_stats;
 
 /* ---- context ------------------------------------------------------------------------ */

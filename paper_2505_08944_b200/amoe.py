@@ -13,8 +13,8 @@ import torch
 
 MAX_G, MAX_E, MAX_GROUP = 8, 256, 128
 BF16, FP32 = 0, 1
-DEFRAG, MTFS, FLFS = 0, 1, 2
-POLICIES = {"defrag": DEFRAG, "mtfs": MTFS, "flfs": FLFS}
+DEFRAG, MTFS, FLFS, SYNC = 0, 1, 2, 3
+POLICIES = {"defrag": DEFRAG, "mtfs": MTFS, "flfs": FLFS, "sync": SYNC}
 BUF = dict(h=0, x=1, pool=2, tok_w=3, tok_idx=4, tok_layer=5, tok_pass=6, rings=7, qctr=8, stats=9, scratch=10)
 STATUS = {0: "OK", 1: "IDLE", 2: "EINVAL", 3: "ENOTHOSTED", 4: "ECUDA", 5: "EDEVICE", 6: "EPEER", 7: "ENOMEM"}
 FAULTS = {1: "ring overflow", 2: "leg count > K+S", 3: "expert index out of range", 4: "not hosted",
@@ -49,7 +49,8 @@ class RunParams(C.Structure):
 
 class RunStats(C.Structure):
     _fields_ = [("picks", C.c_int64), ("queues_run", C.c_int64), ("legs", C.c_int64),
-                ("token_layers", C.c_int64), ("kernel_launches", C.c_int64), ("idle_polls", C.c_int64)]
+                ("token_layers", C.c_int64), ("kernel_launches", C.c_int64), ("idle_polls", C.c_int64),
+                ("idle_ns", C.c_int64), ("wall_ns", C.c_int64), ("barriers", C.c_int64)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}

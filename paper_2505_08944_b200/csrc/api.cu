@@ -17,7 +17,7 @@ namespace amoe {
 int launch_token_init(const DevCtx&, const int32_t*, int, const void*, int, cudaStream_t);
 int launch_enqueue(const DevCtx&, int, const int32_t*, int, const float*, const int32_t*, const float*, cudaStream_t);
 int launch_combine(const DevCtx&, int, cudaStream_t);
-int launch_announce(const DevCtx&, uint32_t, cudaStream_t);
+int launch_announce(const DevCtx&, uint32_t, int, cudaStream_t);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
@@ -55,6 +55,7 @@ struct amoe_ctx {
   int64_t admitted;
   uint64_t retired_base;
   uint32_t epoch;
+  int start_layer = 0;                // layer of the last amoe_enqueue (AMOE_SYNC's first layer)
   cudaStream_t last_stream;
   std::vector<MapCacheEntry> map_cache;
   int32_t* scratch_qinfo;
@@ -358,6 +359,7 @@ amoe_status amoe_enqueue(amoe_ctx_t c, int layer, const int32_t* slots, int T, c
     if (!c->dc.peer[r]) return AMOE_EPEER;
   StageTimer tm(c, ST_ENQUEUE, s);
   c->launches += launch_enqueue(c->dc, layer, slots, T, logits, topk_idx, topk_w, s);
+  c->start_layer = layer;
   c->last_stream = s;
   CK(cudaGetLastError());
   return AMOE_OK;
@@ -611,7 +613,7 @@ amoe_status amoe_get_buffer(amoe_ctx_t c, int which, void** ptr, size_t* bytes) 
 }
 
 amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, amoe_run_stats* stats, void* stream) {
-  if (!c || !p || p->policy < 0 || p->policy > 2 || p->W < 0) return AMOE_EINVAL;
+  if (!c || !p || p->policy < 0 || p->policy > AMOE_SYNC || p->W < 0) return AMOE_EINVAL;
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
   if (!c->dc.router) return AMOE_EINVAL;
@@ -642,14 +644,51 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   const uint64_t retired0 = s0[1], merged0 = s0[0], legs0 = s0[2];
   bool announced = false;
   int idle_streak = 0;
+  // AMOE_SYNC: the layer this rank may run, and whether it has arrived at that layer's barrier
+  const bool sync = p->policy == AMOE_SYNC;
+  int sync_layer = c->start_layer;
+  bool sync_arrived = false;
+  // barrier flag value: (run epoch, barrier index + 1), so ranks agree without shared history
+  auto bar_tag = [&](int64_t b) { return (epoch << 16) | (uint32_t)((b + 1) & 0xffff); };
+  using clk = std::chrono::steady_clock;
+  const auto t_run0 = clk::now();
+  auto finish = [&](amoe_run_stats* out) {
+    rs.wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t_run0).count();
+    if (out) *out = rs;
+  };
   for (;;) {
+    const auto t_poll = clk::now();
     st = snapshot(c, s);
     if (st != AMOE_OK) return st;
     const char* snap = reinterpret_cast<const char*>(c->pinned);
     if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return AMOE_EDEVICE;
     const uint64_t* sv = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
+    if (sync && !announced) {
+      const uint32_t* flags = reinterpret_cast<const uint32_t*>(snap + c->lay.done) + AMOE_MAX_G;
+      if (!sync_arrived && (int64_t)(sv[0] - merged0) >= expected * (int64_t)(rs.barriers + 1) &&
+          (int64_t)(sv[1] - retired0) < expected) {   // the last layer of the run has no barrier
+        // every homed token merged layer sync_layer: arrive at the barrier (flag in every peer)
+        c->launches += launch_announce(c->dc, bar_tag(rs.barriers), AMOE_MAX_G, s);
+        rs.kernel_launches += 1;
+        sync_arrived = true;
+        continue;
+      }
+      if (sync_arrived) {
+        // a rank whose tokens all retired (done == epoch) has nothing left to merge at this layer
+        const uint32_t* done = reinterpret_cast<const uint32_t*>(snap + c->lay.done);
+        bool all = true;
+        for (int r = 0; r < c->cfg.G; ++r)
+          all &= (int32_t)(flags[r] - bar_tag(rs.barriers)) >= 0 || done[r] == epoch;
+        if (all) {   // no leg of sync_layer is left anywhere: take the next layer
+          rs.barriers += 1;
+          sync_layer = (sync_layer + 1) % L;
+          sync_arrived = false;
+          continue;
+        }
+      }
+    }
     if (!announced && (int64_t)(sv[1] - retired0) >= expected) {
-      c->launches += launch_announce(c->dc, epoch, s);
+      c->launches += launch_announce(c->dc, epoch, 0, s);
       rs.kernel_launches += 1;
       announced = true;
       continue;
@@ -665,10 +704,14 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       }
     }
     depths_from_snapshot(c, Q.data());
+    if (sync)   // lockstep: only the current layer's queues are eligible
+      for (int bb = 0; bb < L; ++bb)
+        if (bb != sync_layer) std::fill(Q.begin() + (size_t)bb * H, Q.begin() + (size_t)(bb + 1) * H, 0u);
     const uint32_t* cc = reinterpret_cast<const uint32_t*>(snap + c->lay.cctr);
     const uint32_t cpend = cc[1] - cc[2];
     int b = -1, q = -1;
-    const bool work = pick_queue(Q.data(), L, H, c->cfg.E + c->cfg.S, p->policy, p->W, (double)p->delta, &b, &q) == 0;
+    const int pol = sync ? AMOE_MTFS : p->policy;
+    const bool work = pick_queue(Q.data(), L, H, c->cfg.E + c->cfg.S, pol, p->W, (double)p->delta, &b, &q) == 0;
     if (work) {
       g.nq = 0;
       if (p->grouped) {
@@ -703,17 +746,18 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       idle_streak = 0;
     } else {
       rs.idle_polls += 1;
-      if (c->cfg.G == 1 && !announced) {
+      if (c->cfg.G == 1 && !announced && !sync_arrived) {
         // single GPU: nothing queued and tokens not retired means a lost leg
         rs.token_layers = (int64_t)(sv[0] - merged0);
-        if (stats) *stats = rs;
+        finish(stats);
         return AMOE_EDEVICE;
       }
       if (++idle_streak > 64) std::this_thread::sleep_for(std::chrono::microseconds(5));
+      rs.idle_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t_poll).count();
     }
     if (p->max_picks > 0 && rs.picks >= p->max_picks) break;
   }
-  if (stats) *stats = rs;
+  finish(stats);
   return AMOE_OK;
 }
 

@@ -366,9 +366,12 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 ? 4 : 2)) combine_kerne
   }
 }
 
-__global__ void announce_kernel(DevCtx c, uint32_t epoch) {
+// done[base + rank] = value on every rank (base 0: quiescence epoch; base AMOE_MAX_G: the
+// AMOE_SYNC layer-barrier sequence). Release: the stores of this rank's earlier kernels are
+// visible to a peer that observes the flag.
+__global__ void announce_kernel(DevCtx c, uint32_t value, int base) {
   const int r = threadIdx.x;
-  if (r < c.G) st_release(wsp<uint32_t>(c, r, c.lay.done) + c.rank, epoch, r != c.rank);
+  if (r < c.G) st_release(wsp<uint32_t>(c, r, c.lay.done) + base + c.rank, value, r != c.rank);
 }
 
 // ---------------------------------------------------------------------------- launchers
@@ -435,8 +438,8 @@ int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
   return 2;
 }
 
-int launch_announce(const DevCtx& c, uint32_t epoch, cudaStream_t s) {
-  announce_kernel<<<1, 32, 0, s>>>(c, epoch);
+int launch_announce(const DevCtx& c, uint32_t value, int base, cudaStream_t s) {
+  announce_kernel<<<1, 32, 0, s>>>(c, value, base);
   return 1;
 }
 

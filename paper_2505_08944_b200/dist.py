@@ -88,6 +88,17 @@ def reduce_timing(ms: float, counts, device="cpu", group=None):
     return float(t[0]), [int(round(x)) for x in c.tolist()]
 
 
+def gather_values(vals, device="cpu", group=None):
+    """Per-rank float vectors → [rank][i] on every rank (bench's per-GPU stall report)."""
+    vals = [float(v) for v in vals]
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return [vals]
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [o.tolist() for o in out]
+
+
 def barrier(group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.barrier(group=group)

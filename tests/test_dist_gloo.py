@@ -28,6 +28,8 @@ def _worker(rank, world, port, q):
     D.barrier()
     toks = list(D.token_range(rank, 16))
     hosted = D.hosted_experts(8, 2, world, rank)
+    per_rank = D.gather_values([0.25 * rank, rank + 3])
+    assert per_rank == [[0.25 * r, r + 3.0] for r in range(world)]
     q.put((rank, ms, counts, toks, hosted))
     dist.destroy_process_group()
 

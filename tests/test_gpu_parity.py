@@ -181,7 +181,8 @@ def test_forward_and_combine_bitexact(dtype):
 # ---------------------------------------------------------------- asynchronous loop, end to end
 
 @pytest.mark.parametrize("dtype,policy,grouped", [
-    ("bf16", "defrag", True), ("bf16", "mtfs", False), ("bf16", "flfs", False), ("fp32", "defrag", True)])
+    ("bf16", "defrag", True), ("bf16", "mtfs", False), ("bf16", "flfs", False), ("fp32", "defrag", True),
+    ("bf16", "sync", True), ("bf16", "sync", False)])
 def test_run_tiny_matches_oracle(dtype, policy, grouped):
     P = Problem(**TINY, dtype=dtype, seed=5)
     ctx = P.make_ctx()
@@ -192,6 +193,7 @@ def test_run_tiny_matches_oracle(dtype, policy, grouped):
     ctx.check()
     assert stats["token_layers"] == P.T * P.L * passes
     assert stats["legs"] == P.T * P.L * passes * P.K
+    assert stats["barriers"] == (P.L * passes - 1 if policy == "sync" else 0)
     h_gpu = to_np(ctx.state()["h"])
     W, SH = P.oracle_weights()
     h0 = host_values(P.h0[0], dtype)
@@ -207,14 +209,14 @@ def test_gpu_async_equals_sync_bitwise():
     drain cap) give bit-identical tokens: every row's arithmetic is independent of its batch."""
     P = Problem(**TINY, seed=6)
     outs = []
-    for policy, grouped, cap in (("defrag", True, 0), ("mtfs", False, 0), ("flfs", False, 37)):
+    for policy, grouped, cap in (("defrag", True, 0), ("mtfs", False, 0), ("flfs", False, 37), ("sync", True, 0)):
         ctx = P.make_ctx(max_batch=cap)
         admit(ctx, P)
         ctx.run(retire_pass=2, policy=policy, grouped=grouped)
         torch.cuda.synchronize()
         outs.append(to_np(ctx.state()["h"]))
         ctx.close()
-    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
 def test_shared_experts_and_topk6():
@@ -287,8 +289,8 @@ def test_loopback_peers_match_single_gpu(G):
     assert remote > 0
 
 
-@pytest.mark.parametrize("G,d", [(2, 128), (4, 256)])
-def test_loopback_amoe_run_concurrent_ranks(G, d):
+@pytest.mark.parametrize("G,d,policy", [(2, 128, "defrag"), (4, 256, "defrag"), (2, 128, "sync"), (4, 256, "sync")])
+def test_loopback_amoe_run_concurrent_ranks(G, d, policy):
     """The native multi-rank loop: G contexts on one GPU, each running amoe_run in its own host
     thread on its own CUDA stream, concurrently. Legs cross ranks through peer rings (remote
     reservations race with local producers), outputs return by one-sided stores, and each rank
@@ -310,7 +312,7 @@ def test_loopback_amoe_run_concurrent_ranks(G, d):
     def worker(r):
         try:
             with torch.cuda.stream(streams[r]):
-                stats[r] = ctxs[r].run(retire_pass=2, stream=streams[r])
+                stats[r] = ctxs[r].run(retire_pass=2, policy=policy, stream=streams[r])
         except Exception as e:   # pragma: no cover - reported below
             errs.append((r, e))
 
@@ -325,6 +327,8 @@ def test_loopback_amoe_run_concurrent_ranks(G, d):
     for c in ctxs:
         c.check()
     assert sum(s["token_layers"] for s in stats) == G * T * P.L * 2
+    if policy == "sync":   # lockstep: one box-wide barrier between consecutive layers of the run
+        assert all(s["barriers"] == P.L * 2 - 1 for s in stats), stats
     h = np.concatenate([to_np(c.state()["h"]) for c in ctxs])
     P1 = Problem(L=2, E=8, K=2, S=0, d=d, ff=256, T=G * T, G=1, seed=14)
     P1.tables = [np.concatenate(P.tables, axis=2)]

@@ -29,3 +29,16 @@ def test_weight_scales():
     w1, _, w2 = wl.expert_weights(0, 0, 0, 512, 1024, dtype="fp32")
     assert abs(w1.std() - 512 ** -0.5) < 0.01 * 512 ** -0.5 * 10
     assert abs(w2.std() - 1024 ** -0.5) < 0.01 * 1024 ** -0.5 * 10
+
+
+def test_exponential_skew_variant():
+    """The paper's exponential fit (λ = 0.38 from SPEC.md L164): p_r ∝ e^{-λr}."""
+    p = wl.expon_probs(8, 0.38)
+    assert abs(p.sum() - 1) < 1e-15
+    assert np.allclose(p[:-1] / p[1:], np.exp(0.38), rtol=1e-12)
+    assert np.array_equal(wl.skew_probs(8, "zipf"), wl.zipf_probs(8, 1.2))
+    z = wl.router_logits(0, L=1, T=20000, E=8, skew="exp")[0]
+    top1 = np.bincount(z.argmax(axis=1), minlength=8) / 20000.0
+    perm = wl.layer_perm(0, 0, 0, 8)
+    # argmax of log p + Gumbel is a draw from p: the top-1 share of each expert matches p
+    assert np.abs(top1[perm] - p).max() < 0.015

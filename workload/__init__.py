@@ -12,6 +12,8 @@ from .gen import (  # noqa: F401
     expert_weights,
     router_logits,
     zipf_probs,
+    expon_probs,
+    skew_probs,
     layer_perm,
     skew_epoch,
     CONFIGS,

@@ -74,6 +74,22 @@ def zipf_probs(E: int, s: float) -> np.ndarray:
     return p / p.sum()
 
 
+def expon_probs(E: int, lam: float) -> np.ndarray:
+    """The paper's fitted shape ("fitted ... to an exponential distribution", no λ
+    given; SPEC.md L164 uses λ ≈ 0.38): p_r ∝ exp(-λ r) over ranks r = 0..E-1 (float64)."""
+    p = np.exp(-float(lam) * np.arange(E, dtype=np.float64))
+    return p / p.sum()
+
+
+def skew_probs(E: int, skew: str = "zipf", zipf_s: float = 1.2, lam: float = 0.38) -> np.ndarray:
+    """Rank probabilities of the routing skew: 'zipf' (BASELINE.json) or 'exp' (the paper's fit)."""
+    if skew == "zipf":
+        return zipf_probs(E, zipf_s)
+    if skew == "exp":
+        return expon_probs(E, lam)
+    raise ValueError(f"unknown skew {skew!r}")
+
+
 def skew_epoch(pass_idx: int, l: int, L: int, shift_every: int) -> int:
     """Skew epoch of layer-step (pass, l); a 'step' is one layer traversal by the wave."""
     if shift_every <= 0:
@@ -89,7 +105,7 @@ def layer_perm(seed: int, l: int, epoch: int, E: int, same_perm: bool = False) -
 
 def router_logits(seed: int, L: int, T: int, E: int, zipf_s: float = 1.2, pass_idx: int = 0,
                   shift_every: int = 1000, same_perm: bool = False, layers=None,
-                  token_offset: int = 0) -> np.ndarray:
+                  token_offset: int = 0, skew: str = "zipf", lam: float = 0.38) -> np.ndarray:
     """Synthetic router logits, float32 [len(layers), T, E] for global tokens token_offset..+T.
 
     z[l, t, e] = log p[π_l^-1(e)] + Gumbel(0,1). The Gumbel noise for (pass, l) is drawn for the
@@ -97,7 +113,7 @@ def router_logits(seed: int, L: int, T: int, E: int, zipf_s: float = 1.2, pass_i
     """
     if layers is None:
         layers = range(L)
-    p = zipf_probs(E, zipf_s)
+    p = skew_probs(E, skew, zipf_s, lam)
     out = np.empty((len(layers), T, E), dtype=np.float32)
     for i, l in enumerate(layers):
         perm = layer_perm(seed, l, skew_epoch(pass_idx, l, L, shift_every), E, same_perm)
