@@ -313,6 +313,7 @@ def main():
     launches = ctx.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     prof = ctx.profile_read()
+    execs = ctx.exec_log()
     ctx.profile_enable(False)
     ctx.check()
     token_layers = sum(r["token_layers"] for r in runs)
@@ -348,6 +349,28 @@ def main():
                          "peak_kind": hbm_kind, "algorithmic_bytes": int(nbytes)}
     step_ms = ms / args.steps
 
+    # schedule-conditional roofline: every logged execution of n legs costs
+    # max(6·d·ff·n / F_pk, (6·d·ff + 4·n·d) / BW) (weights streamed once + tile in/out), plus the
+    # combine's algorithmic bytes / BW; t_ideal = all FLOPs / F_pk (charges fragmentation too).
+    f_pk = peak_sust * 1e12
+    bw = hbm_pk * 1e9
+    t_exec = sum(max(6.0 * d * ff * n / f_pk, (6.0 * d * ff + 4.0 * n * d) / bw) for _, _, n in execs)
+    t_act = my_tl * ((K + S) * d * 2 + 3 * d * 2 + E * 4) / bw
+    t_ideal = 6.0 * d * ff * my_legs / f_pk
+    per_rank = D.gather_values([1e3 * (t_exec + t_act), 1e3 * t_ideal], device=dev)
+    t_roof_ms = max(v[0] for v in per_rank)
+    t_ideal_ms = max(v[1] for v in per_rank)
+    hist = {}
+    for _, _, n in execs:
+        b = 1 << max(0, int(n).bit_length() - 1)
+        hist[b] = hist.get(b, 0) + 1
+    step_roof = {"t_roof_ms": round(t_roof_ms, 3), "t_ideal_ms": round(t_ideal_ms, 3), "measured_ms": round(ms, 3),
+                 "frac_of_schedule_roofline": round(t_roof_ms / ms, 4), "frac_of_ideal": round(t_ideal_ms / ms, 4),
+                 "peaks": f"{peak_sust} TFLOP/s ({peak_kind.split(':')[0]}), {hbm_pk} GB/s ({hbm_kind})",
+                 "executions_rank0": len(execs),
+                 "mean_legs_per_execution_rank0": round(my_legs / max(1, len(execs)), 1),
+                 "legs_per_execution_hist_rank0": {f">={k}": v for k, v in sorted(hist.items())}}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -368,7 +391,8 @@ def main():
                      "ffn_tflops": (6.0 * d * ff * my_legs / ((gu_ms + dn_ms) / 1e3) / 1e12) if gu_ms else None,
                      "stage_ms_total": stage_ms,
                      "stage_launches": {k: v[1] for k, v in prof.items()},
-                     "hbm_kernels": hbm},
+                     "hbm_kernels": hbm,
+                     "step": step_roof},
     }
 
     # ------------------------------------------------------------------ end to end (host buffers)

@@ -252,6 +252,11 @@ amoe_status amoe_pass_host(amoe_ctx_t ctx, const void* h0_host, const float* rou
  * [3] forward, [4] combine (+route/scatter), [5] token_init/enqueue, [6..7] reserved. */
 amoe_status amoe_profile_enable(amoe_ctx_t ctx, int enable);
 amoe_status amoe_profile_read(amoe_ctx_t ctx, double ms_out[8], int64_t counts_out[8]);
+/* Expert executions amoe_run performed while profiling was enabled (reset by
+ * amoe_profile_enable): pairs out[2i] = layer * H + local queue, out[2i+1] = legs drained by that
+ * execution (taken from consecutive ring-head snapshots, so exact). Copies min(cap, *n_out)
+ * pairs; *n_out = executions logged. For the schedule-conditional roofline. */
+amoe_status amoe_exec_log(amoe_ctx_t ctx, int32_t* out, int cap, int* n_out);
 
 /* ---- introspection -------------------------------------------------------------------- */
 

@@ -81,6 +81,7 @@ EXPORTS = {
                                  C.POINTER(RunStats), C.c_void_p]),
     "amoe_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "amoe_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "amoe_exec_log": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_int)]),
     "amoe_get_buffer": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     "amoe_hosted": (C.c_int, [C.c_void_p]),
     "amoe_ring_cap": (C.c_int, [C.c_void_p]),
@@ -328,6 +329,15 @@ class Context:
         ms, n = (C.c_double * 8)(), (C.c_int64 * 8)()
         self._chk(self.lib.amoe_profile_read(self.h, ms, n), "amoe_profile_read")
         return {s: (float(ms[i]), int(n[i])) for i, s in enumerate(self.STAGES)}
+
+    def exec_log(self):
+        """[(layer, local queue, legs)] of every execution amoe_run performed while profiling."""
+        n = C.c_int()
+        self._chk(self.lib.amoe_exec_log(self.h, None, 0, C.byref(n)), "amoe_exec_log")
+        buf = (C.c_int32 * (2 * max(1, n.value)))()
+        self._chk(self.lib.amoe_exec_log(self.h, buf, n.value, C.byref(n)), "amoe_exec_log")
+        H = self.H
+        return [(buf[2 * i] // H, buf[2 * i] % H, buf[2 * i + 1]) for i in range(n.value)]
 
     # -- introspection
     def buffer(self, name, dtype=None, shape=None):

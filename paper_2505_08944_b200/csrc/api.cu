@@ -66,6 +66,9 @@ struct amoe_ctx {
   std::vector<Rec> recs;
   double prof_ms[8] = {0};
   int64_t prof_n[8] = {0};
+  // executions logged by amoe_run while profiling: (l*H + q, drained legs), from the ring heads
+  std::vector<uint32_t> prev_head;
+  std::vector<int32_t> exec_log;
 };
 
 enum Stage { ST_REBATCH = 0, ST_GATEUP = 1, ST_DOWN = 2, ST_FORWARD = 3, ST_COMBINE = 4, ST_ENQUEUE = 5 };
@@ -371,6 +374,23 @@ static amoe_status snapshot(amoe_ctx* c, cudaStream_t s) {
   return AMOE_OK;
 }
 
+// Executions since the previous snapshot: a queue's consumer head only moves when a pick drains
+// it, and one poll launches at most one pick (each queue at most once), so every head delta
+// between consecutive snapshots is exactly one execution of that many legs.
+static void log_executions(amoe_ctx* c, bool reset) {
+  const uint32_t* q = c->pinned + c->lay.qctr / 4;
+  const int n = c->cfg.L * c->H;
+  c->prev_head.resize(n);
+  for (int i = 0; i < n; ++i) {
+    const uint32_t h = q[4 * i + 2];
+    if (!reset && c->prof && h != c->prev_head[i]) {
+      c->exec_log.push_back(i);
+      c->exec_log.push_back((int32_t)(h - c->prev_head[i]));
+    }
+    c->prev_head[i] = h;
+  }
+}
+
 static void depths_from_snapshot(amoe_ctx* c, uint32_t* Q) {
   const uint32_t* q = c->pinned + c->lay.qctr / 4;
   const int n = c->cfg.L * c->H;
@@ -640,6 +660,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   std::vector<uint32_t> Q((size_t)L * H);
   amoe_status st = snapshot(c, s);
   if (st != AMOE_OK) return st;
+  log_executions(c, true);
   const uint64_t* s0 = reinterpret_cast<const uint64_t*>(reinterpret_cast<const char*>(c->pinned) + c->lay.stats);
   const uint64_t retired0 = s0[1], merged0 = s0[0], legs0 = s0[2];
   bool announced = false;
@@ -663,6 +684,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
     const char* snap = reinterpret_cast<const char*>(c->pinned);
     if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return AMOE_EDEVICE;
     const uint64_t* sv = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
+    log_executions(c, false);
     if (sync && !announced) {
       const uint32_t* flags = reinterpret_cast<const uint32_t*>(snap + c->lay.done) + AMOE_MAX_G;
       if (!sync_arrived && (int64_t)(sv[0] - merged0) >= expected * (int64_t)(rs.barriers + 1) &&
@@ -797,6 +819,15 @@ amoe_status amoe_profile_enable(amoe_ctx_t c, int enable) {
   c->recs.clear();
   for (int i = 0; i < 8; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
   c->prof = enable != 0;
+  c->exec_log.clear();
+  return AMOE_OK;
+}
+
+amoe_status amoe_exec_log(amoe_ctx_t c, int32_t* out, int cap, int* n_out) {
+  if (!c || !n_out || cap < 0 || (cap > 0 && !out)) return AMOE_EINVAL;
+  const int n = (int)(c->exec_log.size() / 2);
+  *n_out = n;
+  std::copy(c->exec_log.begin(), c->exec_log.begin() + 2 * (size_t)std::min(n, cap), out);
   return AMOE_OK;
 }
 

@@ -366,3 +366,25 @@ def test_empty_group_is_a_noop():
     torch.cuda.synchronize()
     ctx.check()
     assert gb.info()[0].sum() == 0
+
+
+def test_exec_log_accounts_for_every_leg():
+    """amoe_exec_log (the schedule-conditional roofline's input): while profiling, every
+    execution's drained-leg count is logged; they sum to the legs run, per (layer, queue) to the
+    router histogram of that layer."""
+    P = Problem(**TINY, seed=8)
+    ctx = P.make_ctx()
+    admit(ctx, P)
+    ctx.profile_enable(True)
+    stats = ctx.run(retire_pass=1, policy="mtfs", grouped=False)
+    torch.cuda.synchronize()
+    log = ctx.exec_log()
+    ctx.profile_enable(False)
+    assert len(log) == stats["queues_run"]
+    assert sum(n for _, _, n in log) == stats["legs"] == P.T * P.L * P.K
+    qctr = ctx.state()["qctr"].cpu().numpy()
+    per_q = np.zeros(qctr.shape[:2], dtype=np.int64)
+    for l, q, n in log:
+        assert n > 0
+        per_q[l, q] += n
+    assert np.array_equal(per_q, qctr[..., 2].astype(np.int64))
