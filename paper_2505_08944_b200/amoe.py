@@ -21,7 +21,8 @@ FAULTS = {1: "ring overflow", 2: "leg count > K+S", 3: "expert index out of rang
           5: "combine ring overflow", 6: "token slot out of range", 7: "stale/unpublished ring entry",
           8: "no router table"}
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libamoe.so")
+# AMOE_LIB: load another build of the same library (A/B measurements of two builds in one run)
+LIB_PATH = os.environ.get("AMOE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libamoe.so")
 
 
 class Config(C.Structure):

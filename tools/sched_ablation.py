@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--config", default="mixtral")
     ap.add_argument("--passes", type=int, default=2)
     ap.add_argument("--T", type=int, default=0)
-    ap.add_argument("--policies", default="defrag,mtfs,flfs")
+    ap.add_argument("--policies", default="defrag,mtfs,flfs,sync")
     ap.add_argument("--starts", default="wave,spread")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -71,6 +71,8 @@ def main():
     rows = []
     for kind in args.starts.split(","):
         for policy in args.policies.split(","):
+            if policy == "sync" and kind != "wave":
+                continue            # lockstep layers need every token at the same layer
             for grouped in (True, False):
                 # warm-up (same configuration, one pass)
                 start(kind)
