@@ -15,7 +15,7 @@ constexpr int kWarp = 32;
 constexpr int kMaxKS = 12;          // K + S legs per token
 constexpr int kRowAlign = 128;      // group rows are allocated per queue in multiples of this
 constexpr int kSplitSlots = 512;    // split-K tile slots (counters)
-constexpr int kSplitUnits = 496;    // split-K partial tiles (128 x 256 fp32 each): 62 MB
+constexpr int kSplitUnits = 2048;   // split-K partial tiles (128 x 256 fp32 each): 256 MB
 
 // Device fault codes latched into the error word.
 enum Fault : uint32_t {

@@ -374,17 +374,24 @@ __device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx&
   // the fixed-order reduction and the final stores run in splitk_reduce_kernel (stream-ordered)
 }
 
-// Device-side split decision (identical in every CTA): split K only when the output tiles
-// cannot occupy the tile slots (CTAs or CTA pairs); >= 4 K blocks per unit, <= 2 units per slot.
-// halves = split-K slots per tile (2 for a CTA pair: each CTA reduces its own 128 rows).
-// Only the cold regime splits (every queue fits one M tile: weight streaming dominates and the
-// fp32 partials are small); units keep >= 8 K blocks and aim at ~4 per tile slot.
-__device__ __forceinline__ int choose_split(const FfnArgs& a, int tiles, int slots, int halves, int max_m_tiles) {
-  if (!a.allow_split || tiles <= 0 || max_m_tiles > 1 || tiles >= 2 * slots || tiles * halves > kSplitSlots) return 1;
-  int s = (4 * slots + tiles - 1) / tiles;
+// Device-side split decision (identical in every CTA and in splitk_reduce_kernel). Split K only
+// in the cold regime — every queue fits one M tile, so weight streaming dominates — and only when
+// slots (CTAs or CTA pairs) would idle: fewer output tiles than slots, or up to 1.25x as many when
+// the unit's fp32 partial rows are tiny (<= 16 rows per half). halves = split-K slots per tile
+// (2 for a CTA pair: each CTA reduces its own 128 rows). ~3 units per slot, >= 8 K blocks per
+// unit, and each unit's partial rows (rows x 1 KB) <= 1/4 of the weight bytes it streams (16 KB
+// per K block per CTA): s <= 4·kb / rows. Tuned with tools/rebatch_sweep.py A/B runs
+// (profiles/r01_rebatch_sweep.md): splitting with tiles >= slots, or heavy partials, was slower.
+__device__ __forceinline__ int choose_split(const FfnArgs& a, int tiles, int slots, int halves, int max_m_tiles,
+                                            int max_n) {
+  if (!a.allow_split || tiles <= 0 || max_m_tiles > 1 || tiles * halves > kSplitSlots) return 1;
+  const int rows = max(1, (max_n + halves - 1) / halves);
+  if (!(tiles < slots || (4 * tiles < 5 * slots && rows <= 16))) return 1;
+  int s = (3 * slots + tiles - 1) / tiles;
   s = min(s, a.k_blocks / 8);
   s = min(s, 32);
   s = min(s, kSplitUnits / (tiles * halves));
+  s = min(s, 4 * a.k_blocks / rows);
   return max(s, 1);
 }
 
@@ -427,6 +434,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
     s_pre[nq] = acc;
     s_start[AMOE_MAX_GROUP] = mm;
+    int mn = 0;
+    for (int q = 0; q < nq; ++q) mn = max(mn, s_n[q]);
+    s_start[AMOE_MAX_GROUP + 1] = mn;
     s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES + s]), 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(smem_u32(&bars[2 * STAGES + a]), 1); mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 1); }
@@ -444,7 +454,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const uint32_t tmem_base = *tmem_holder;
   Sched sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_off, s_pre};
   const int kb_n = args.k_blocks;
-  const int split = choose_split(args, sc.total, gridDim.x, 1, s_start[AMOE_MAX_GROUP]);
+  const int split = choose_split(args, sc.total, gridDim.x, 1, s_start[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP + 1]);
   const int units = sc.total * split;
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
@@ -692,6 +702,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     }
     s_pre[nq] = acc;
     s_start[AMOE_MAX_GROUP] = mm;
+    int mn = 0;
+    for (int q = 0; q < nq; ++q) mn = max(mn, s_n[q]);
+    s_start[AMOE_MAX_GROUP + 1] = mn;
     s_fwd[0] = 0; s_fwd[1] = 0;
     for (int s = 0; s < STAGES2; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES2 + s]), 1); }
     for (int a = 0; a < 2; ++a) {
@@ -713,7 +726,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   Sched2 sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_pre};
   const int kb_n = args.k_blocks;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int split = choose_split(args, sc.total, ncl, 2, s_start[AMOE_MAX_GROUP]);
+  const int split = choose_split(args, sc.total, ncl, 2, s_start[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP + 1]);
   const int units = sc.total * split;
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
@@ -850,7 +863,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
   constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;        // partial row width (fp32)
   constexpr int CPL = (MODE == MODE_GATEUP ? 128 : BN) / 32;  // output columns per lane
   __shared__ int s_n[AMOE_MAX_GROUP], s_off[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP], s_pre[AMOE_MAX_GROUP + 1];
-  __shared__ int s_mmax;
+  __shared__ int s_mmax, s_nmax;
   __shared__ int s_rpre[AMOE_MAX_GROUP + 1];   // prefix of valid (tile, row) items per queue
   const int nq = args.nq;
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
@@ -865,13 +878,16 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
     }
     s_pre[nq] = acc;
     s_mmax = mm;
+    int mn = 0;
+    for (int q = 0; q < nq; ++q) mn = max(mn, s_n[q]);
+    s_nmax = mn;
     int ri = 0;
     for (int q = 0; q < nq; ++q) { s_rpre[q] = ri; ri += s_n[q] * args.n_tiles; }
     s_rpre[nq] = ri;
   }
   __syncthreads();
   const int total = s_pre[nq];
-  const int split = choose_split(args, total, slots, HALVES, s_mmax);
+  const int split = choose_split(args, total, slots, HALVES, s_mmax, s_nmax);
   if (split <= 1) return;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
