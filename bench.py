@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--router", default="table", choices=["table", "gate"],
+                    help="table: synthetic Zipf logits (the paper's eval); gate: device router gate "
+                         "x·Wgᵀ + per-layer Zipf log-prob bias computed in the combine (SURVEY.md f3)")
     ap.add_argument("--skew", default="zipf", choices=["zipf", "exp"],
                     help="routing skew: Zipf s=1.2 (BASELINE.json) or the paper's exponential fit (λ=0.38)")
     return ap.parse_args()
@@ -56,12 +59,12 @@ def FFN_KERNEL(d):
     return "ffn_tc_kernel<GATEUP> (tcgen05 UMMA 128x256, fused SwiGLU)"
 
 
-def config_dict(spec, L, T, G, policy, grouped, skew="zipf"):
+def config_dict(spec, L, T, G, policy, grouped, skew="zipf", router="table"):
     """The workload description shared by both arms' JSON lines."""
     return {"workload": f"{spec.name}-shaped expert layers: L={L} E={spec.E} top-{spec.K} S={spec.S} d={spec.d} "
                         f"ff={spec.ff}, {T} tokens in flight per GPU, "
                         + (f"Zipf s={spec.zipf_s}" if skew == "zipf" else "exponential λ=0.38") + " routing",
-            "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped,
+            "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped, "router": router,
             "l2": "inputs larger than L2 (resident weights >> 126 MB); no flush",
             "step": "one decode pass: every token through all L layers"}
 
@@ -272,6 +275,14 @@ def main():
                    for p in range(n_tab)]
     table = torch.from_numpy(np.stack(tables_host)).to(dev).contiguous()
     ctx.set_router(table)
+    gate_w = []
+    if args.router == "gate":
+        for l in range(L):
+            wg = torch.empty(E, d, dtype=torch.bfloat16, device=dev).normal_(0, d ** -0.5, generator=gen)
+            perm = torch.from_numpy(wl.layer_perm(args.seed, l, 0, E).argsort()).to(dev)
+            bias = torch.from_numpy(np.log(wl.skew_probs(E, args.skew, spec.zipf_s))).float().to(dev)[perm].contiguous()
+            ctx.set_gate(l, wg, bias)
+            gate_w.append((wg, bias))
     h0 = torch.from_numpy(wl.hidden0(args.seed, T, d, token_offset=rank * T).view(np.int16)).view(
         torch.bfloat16).to(dev)
     slots = torch.arange(T, dtype=torch.int32, device=dev)
@@ -280,7 +291,10 @@ def main():
 
     def step(p):
         ctx.token_init(slots, h0, p)
-        ctx.enqueue(0, slots, logits=table[p % n_tab, 0])
+        if args.router == "gate":
+            ctx.enqueue(0, slots)
+        else:
+            ctx.enqueue(0, slots, logits=table[p % n_tab, 0])
         return ctx.run(retire_pass=p + 1, policy=policy, grouped=grouped)
 
     barrier = D.barrier
@@ -375,7 +389,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
-        "config": config_dict(spec, L, T, G, policy, grouped, args.skew),
+        "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router),
         "gpu_launches": int(launches),
         "clocks": clk,
         "stall": {"idle_frac_per_rank": [round(v[0], 4) for v in stall], "layer_barriers": int(stall[0][1]),

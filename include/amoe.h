@@ -169,6 +169,15 @@ amoe_status amoe_set_expert(amoe_ctx_t ctx, int layer, int expert, const void* w
  * [n_tables][L][T_slots][E]; a token at (pass p, layer l) uses table p mod n_tables. */
 amoe_status amoe_set_router(amoe_ctx_t ctx, const float* table, int n_tables);
 
+/* Router gate of `layer` (the gate is the last op of the attention layer,
+ * PAPER.md L175, L227): logits z[e] = Σ_j x[j]·wg[e][j] (+ bias[e]), fp32 accumulation, on the
+ * token's x = rmsnorm(h) at that layer, then the same top-K + softmax as table routing. wg:
+ * device [E][d] storage dtype, row-major; bias: device fp32 [E] or NULL. Borrowed. A layer with
+ * a gate routes with it (in amoe_combine, and in amoe_enqueue when logits and topk_* are NULL);
+ * other layers use the router table. wg = NULL clears the layer's gate. EINVAL when d exceeds
+ * 4096 (bf16) / 2048 (fp32). Synchronous (16-byte H2D copy). */
+amoe_status amoe_set_gate(amoe_ctx_t ctx, int layer, const void* wg, const float* bias);
+
 /* Admit tokens: for i < T, slot = slots[i] (device int32): h[slot] = h0[i] (device [T, d]
  * storage dtype), x[slot] = rmsnorm(h0[i]), pass = pass, layer = 0, pool cleared. */
 amoe_status amoe_token_init(amoe_ctx_t ctx, const int32_t* slots, int T, const void* h0, int pass,
@@ -239,7 +248,8 @@ amoe_status amoe_run(amoe_ctx_t ctx, const amoe_run_params* params, int retire_p
 
 /* One decode pass end-to-end from HOST buffers: h0_host [T_slots, d] storage dtype (all slots)
  * is copied in, and router_host [L][T_slots][E] fp32 (or NULL to keep the resident table) is
- * copied into router table (pass mod n_tables); every token runs layers 0..L-1 once
+ * copied into router table (pass mod n_tables; layer 0 routes with its gate instead when
+ * amoe_set_gate gave it one); every token runs layers 0..L-1 once
  * (amoe_token_init + amoe_enqueue(layer 0) + amoe_run) and the final h is copied to
  * h_out_host [T_slots, d]. Synchronises `stream`. Multi-GPU: every rank calls it. */
 amoe_status amoe_pass_host(amoe_ctx_t ctx, const void* h0_host, const float* router_host, void* h_out_host,

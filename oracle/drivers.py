@@ -21,18 +21,23 @@ from . import scheduler as sch
 from .queues import Box
 
 
-def sync_run(h0, logits_fn, weights, K, n_passes=1, shared=None, dtype="bf16", record=False):
+def sync_run(h0, logits_fn, weights, K, n_passes=1, shared=None, dtype="bf16", record=False, gates=None):
     """Fixed-batch EP semantics: every token through layer l, then l+1.
 
     h0 [N, d] storage values (fp32 array); logits_fn(pass, l) -> [N, E] fp32;
-    weights[l][e] = (w1, w3, w2); shared[l][j] likewise or None.
+    weights[l][e] = (w1, w3, w2); shared[l][j] likewise or None; gates[l] = (wg [E, d], bias
+    [E] or None) routes layer l with the gate on x_l = rmsnorm(h) instead of logits_fn.
     Returns final h and (if record) the per-(pass, layer) dicts of numerics.moe_layer."""
     h = np.asarray(h0, dtype=np.float32)
     L = len(weights)
     recs = []
     for p in range(n_passes):
         for l in range(L):
-            r = nx.moe_layer(h, logits_fn(p, l), weights[l], K,
+            if gates is not None and gates[l] is not None:
+                z = nx.gate_logits(nx.rmsnorm(h, dtype), *gates[l])
+            else:
+                z = logits_fn(p, l)
+            r = nx.moe_layer(h, z, weights[l], K,
                              shared[l] if shared else (), dtype)
             if record:
                 recs.append(r)

@@ -77,6 +77,15 @@ def route_topk(z: np.ndarray, K: int):
     return idx, w
 
 
+def gate_logits(x: np.ndarray, wg: np.ndarray, bias: np.ndarray | None = None) -> np.ndarray:
+    """Router gate ("gating" is the last op of the attention layer, PAPER.md
+    L175): z[t, e] = Σ_j x[t, j]·wg[e, j] + bias[e], accumulated in float64, rounded to fp32."""
+    z = np.asarray(x, np.float64) @ np.asarray(wg, np.float64).T
+    if bias is not None:
+        z = z + np.asarray(bias, np.float64)[None, :]
+    return z.astype(np.float32)
+
+
 # ----------------------------------------------------------------------------- a5-a6: expert
 
 

@@ -63,6 +63,7 @@ EXPORTS = {
     "amoe_import_peers": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
     "amoe_set_expert": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "amoe_set_router": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "amoe_set_gate": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "amoe_token_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     "amoe_enqueue": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p]),
@@ -254,6 +255,15 @@ class Context:
         self._router = table
         n_tab = table.numel() // (self.L * self.T * self.E)
         self._chk(self.lib.amoe_set_router(self.h, _p(table), n_tab), "amoe_set_router")
+
+    def set_gate(self, layer, wg: torch.Tensor | None, bias: torch.Tensor | None = None):
+        """Router gate of `layer` (logits = x·wgᵀ + bias): wg [E, d] storage dtype, bias fp32 [E]."""
+        if wg is not None:
+            assert wg.is_contiguous() and tuple(wg.shape) == (self.E, self.d)
+            assert bias is None or (bias.dtype == torch.float32 and bias.numel() == self.E)
+        self._gates = getattr(self, "_gates", {})
+        self._gates[layer] = (wg, bias)         # borrowed by the library: keep alive
+        self._chk(self.lib.amoe_set_gate(self.h, layer, _p(wg), _p(bias)), "amoe_set_gate")
 
     def local_queue(self, expert):
         return self.lib.amoe_local_queue(self.h, expert)

@@ -27,7 +27,7 @@ enum Fault : uint32_t {
   F_CRING_OVERFLOW = 5,   // args: reserve, head
   F_SLOT_RANGE = 6,       // args: slot, T
   F_STALE_ENTRY = 7,      // args: queue, position, seq
-  F_NO_ROUTER = 8,        // args: slot, layer, pass (combine needs amoe_set_router)
+  F_NO_ROUTER = 8,        // args: slot, layer, pass (needs amoe_set_router or amoe_set_gate)
 };
 
 // Byte offsets of every object inside a rank's workspace. Identical on every rank (the
@@ -51,6 +51,7 @@ struct Layout {
   uint64_t tok_idx;    // i32[T][K]
   uint64_t wmaps;      // CUtensorMap[L*H][3]
   uint64_t wptrs;      // u64[L*H][3]
+  uint64_t gate;       // u64[L][2]: router gate weights [E][d] (storage dtype) and bias [E] fp32, or 0
   uint64_t s_tile, s_meta, s_qinfo, s_act, s_out;   // amoe_run's group scratch
   uint64_t split_part; // f32 split-K partials: kSplitUnits x 128 rows x 256 columns
   uint64_t total;
@@ -65,6 +66,8 @@ struct DevCtx {
   float eps;
   int32_t n_tab;
   const float* router;               // local [n_tab][L][T][E] or null
+  int32_t gate_on;                   // some layer has a router gate (amoe_set_gate)
+  int32_t pad_gate;
   Layout lay;
   uint64_t peer[AMOE_MAX_G];         // workspace base per rank; peer[rank] = local
   int16_t lq[AMOE_MAX_E];            // local queue index of routed expert e on its owner

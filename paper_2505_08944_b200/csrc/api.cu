@@ -55,6 +55,7 @@ struct amoe_ctx {
   int64_t admitted;
   uint64_t retired_base;
   uint32_t epoch;
+  std::vector<char> gate_set;         // [L] layer has a router gate (amoe_set_gate)
   int start_layer = 0;                // layer of the last amoe_enqueue (AMOE_SYNC's first layer)
   cudaStream_t last_stream;
   std::vector<MapCacheEntry> map_cache;
@@ -192,6 +193,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->tok_idx = take(T * c->K * 4);
   L->wmaps = take((uint64_t)c->L * H * 3 * 128, 128);
   L->wptrs = take((uint64_t)c->L * H * 3 * 8);
+  L->gate = take((uint64_t)c->L * 16);
   L->s_qinfo = take(3 * AMOE_MAX_GROUP * 4);
   L->s_meta = take((uint64_t)rows * 16);
   L->s_tile = take((uint64_t)rows * d * es, 1024);
@@ -335,6 +337,19 @@ amoe_status amoe_set_expert(amoe_ctx_t c, int layer, int expert, const void* w1,
   return AMOE_OK;
 }
 
+amoe_status amoe_set_gate(amoe_ctx_t c, int layer, const void* wg, const float* bias) {
+  if (!c || layer < 0 || layer >= c->cfg.L) return AMOE_EINVAL;
+  // the gate keeps the token's x row in registers: 16 chunks of 16 B per lane
+  if (wg && c->cfg.d > 16 * 32 * (16 / (int)c->dc.esize)) return AMOE_EINVAL;
+  const uint64_t v[2] = {reinterpret_cast<uint64_t>(wg), wg ? reinterpret_cast<uint64_t>(bias) : 0};
+  CK(cudaMemcpy(c->ws + c->lay.gate + (uint64_t)layer * 16, v, 16, cudaMemcpyHostToDevice));
+  c->gate_set.resize(c->cfg.L, 0);
+  c->gate_set[layer] = wg != nullptr;
+  c->dc.gate_on = 0;
+  for (char g : c->gate_set) c->dc.gate_on |= g;
+  return AMOE_OK;
+}
+
 amoe_status amoe_set_router(amoe_ctx_t c, const float* table, int n_tables) {
   if (!c || !table || n_tables < 1) return AMOE_EINVAL;
   c->dc.router = table;
@@ -356,7 +371,9 @@ amoe_status amoe_token_init(amoe_ctx_t c, const int32_t* slots, int T, const voi
 amoe_status amoe_enqueue(amoe_ctx_t c, int layer, const int32_t* slots, int T, const float* logits,
                          const int32_t* topk_idx, const float* topk_w, void* stream) {
   if (!c || T < 0 || layer < 0 || layer >= c->cfg.L) return AMOE_EINVAL;
-  if (T > 0 && (!slots || (!logits && (!topk_idx || !topk_w)))) return AMOE_EINVAL;
+  // no logits and no (idx, w): route with the layer's gate (amoe_set_gate) on the tokens' x
+  if (T > 0 && (!slots || (!logits && (!topk_idx || !topk_w) && !c->dc.gate_on))) return AMOE_EINVAL;
+  if (!logits && (!topk_idx || !topk_w)) { topk_idx = nullptr; topk_w = nullptr; }
   cudaStream_t s = (cudaStream_t)stream;
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
@@ -636,7 +653,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   if (!c || !p || p->policy < 0 || p->policy > AMOE_SYNC || p->W < 0) return AMOE_EINVAL;
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
-  if (!c->dc.router) return AMOE_EINVAL;
+  if (!c->dc.router && !c->dc.gate_on) return AMOE_EINVAL;
   for (size_t i = 0; i < c->hosted_flags.size(); ++i)
     if (!c->hosted_flags[i]) {
       // every hosted queue needs weights (routed experts of this rank and the shared experts)
@@ -785,7 +802,9 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
 
 amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, const float* router_host, void* h_out_host, int pass,
                            const amoe_run_params* p, amoe_run_stats* stats, void* stream) {
-  if (!c || !h0_host || !h_out_host || !p || !c->dc.router) return AMOE_EINVAL;
+  const bool gate0 = c && !c->gate_set.empty() && c->gate_set[0];
+  if (!c || !h0_host || !h_out_host || !p || (!c->dc.router && !gate0)) return AMOE_EINVAL;
+  if (router_host && !c->dc.router) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = (size_t)c->cfg.T_slots * c->cfg.d * c->dc.esize;
   // all slots, identity order: the slot list lives in the scratch meta area head (int32 iota)
@@ -803,7 +822,9 @@ amoe_status amoe_pass_host(amoe_ctx_t c, const void* h0_host, const float* route
   }
   amoe_status st = amoe_token_init(c, slots, c->cfg.T_slots, c->ws + c->lay.h, pass, s);
   if (st != AMOE_OK) return st;
-  const float* z0 = c->dc.router + (uint64_t)(pass % c->dc.n_tab) * c->cfg.L * c->cfg.T_slots * c->cfg.E;
+  // layer 0 routes with its gate when it has one, else from the router table
+  const float* z0 = gate0 ? nullptr
+                          : c->dc.router + (uint64_t)(pass % c->dc.n_tab) * c->cfg.L * c->cfg.T_slots * c->cfg.E;
   if ((st = amoe_enqueue(c, 0, slots, c->cfg.T_slots, z0, nullptr, nullptr, s)) != AMOE_OK) return st;
   CK(cudaStreamSynchronize(s));   // the slot list area is reused as scratch by amoe_run
   if ((st = amoe_run(c, p, pass + 1, stats, s)) != AMOE_OK) return st;

@@ -67,6 +67,51 @@ __device__ __forceinline__ void route_select(const float (&v)[kZJ], int E, int K
   my_w = lane < K ? ex / sum : 0.f;
 }
 
+// Router gate: z[e] = Σ_j x[j]·wg[e][j] (+ bias[e]) for the token row x
+// (storage T, already stored by this warp), fp32 accumulation (per lane over its 16-B chunks in
+// column order, then the xor-tree warp sum). The row stays in registers (<= 16 chunks per lane);
+// lane e % 32 receives z[e] in v[e / 32], the layout route_select expects.
+template <typename T>
+__device__ __forceinline__ void gate_logits(const DevCtx& c, const T* __restrict__ x, const T* __restrict__ wg,
+                                            const float* __restrict__ bias, int lane, float (&v)[kZJ]) {
+  using V = Vec<T>;
+  constexpr int MAXC = 16;
+  uint4 xr[MAXC];
+#pragma unroll
+  for (int i = 0; i < MAXC; ++i) {
+    const int col = (i * kWarp + lane) * V::N;
+    if (col < c.d) xr[i] = *reinterpret_cast<const uint4*>(x + col);
+  }
+#pragma unroll
+  for (int j = 0; j < kZJ; ++j) v[j] = -INFINITY;
+#pragma unroll 1
+  for (int e = 0; e < c.E; ++e) {
+    const T* w = wg + (uint64_t)e * c.d;
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int col = (i * kWarp + lane) * V::N;
+      if (col < c.d) {
+        float xf[V::N], wf[V::N];
+        V::unpack(xr[i], xf);
+        V::unpack(*reinterpret_cast<const uint4*>(w + col), wf);
+#pragma unroll
+        for (int q = 0; q < V::N; ++q) acc = fmaf(xf[q], wf[q], acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (bias) acc += bias[e];
+#pragma unroll
+    for (int j = 0; j < kZJ; ++j)
+      if (e == j * kWarp + lane) v[j] = acc;
+  }
+}
+
+// The gate of `layer`, or (nullptr, nullptr) when the layer routes from the table.
+__device__ __forceinline__ const uint64_t* gate_entry(const DevCtx& c, int layer) {
+  return wsp<uint64_t>(c, c.rank, c.lay.gate) + 2 * (uint64_t)layer;
+}
+
 // ---------------------------------------------------------------------------- scatter (a2)
 // Every thread of the CTA calls this. Legs with r >= 0 are appended to ring (r, q): one
 // reservation atomic per (warp, queue) (__match_any_sync aggregation), entries written with
@@ -211,6 +256,19 @@ __global__ void __launch_bounds__(kTokThreads) enqueue_kernel(DevCtx c, int laye
         float zv[kZJ];
         route_load(logits + (uint64_t)i * c.E, c.E, lane, zv);
         route_select(zv, c.E, c.K, lane, my_e, my_w);
+      } else if (!tidx) {
+        // gate routing on the token's x (amoe_set_gate); no gate for this layer is a fault
+        const uint64_t* ge = gate_entry(c, layer);
+        if (!ge[0]) { if (lane == 0) raise_fault(c, F_NO_ROUTER, slot, layer, 0); continue; }
+        float zv[kZJ];
+        if (c.dtype == AMOE_BF16)
+          gate_logits<__nv_bfloat16>(c, wsp<__nv_bfloat16>(c, c.rank, c.lay.x) + (uint64_t)slot * c.d,
+                                     reinterpret_cast<const __nv_bfloat16*>(ge[0]),
+                                     reinterpret_cast<const float*>(ge[1]), lane, zv);
+        else
+          gate_logits<float>(c, wsp<float>(c, c.rank, c.lay.x) + (uint64_t)slot * c.d,
+                             reinterpret_cast<const float*>(ge[0]), reinterpret_cast<const float*>(ge[1]), lane, zv);
+        route_select(zv, c.E, c.K, lane, my_e, my_w);
       } else if (lane < c.K) {
         my_e = tidx[(uint64_t)i * c.K + lane];
         my_w = tw[(uint64_t)i * c.K + lane];
@@ -267,8 +325,8 @@ __global__ void cdrain_kernel(DevCtx c) {
 // ---------------------------------------------------------------------------- combine (a8)
 
 // KSM: compile-time bound on K+S (2, 4, 8 or 12) sizing the per-chunk leg registers.
-template <typename T, int KSM>
-__global__ void __launch_bounds__(kTokThreads, (KSM <= 4 ? 4 : 2)) combine_kernel(DevCtx c, int retire_pass) {
+template <typename T, int KSM, bool GATE>
+__global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) combine_kernel(DevCtx c, int retire_pass) {
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   __shared__ unsigned long long s_merged, s_retired;
@@ -303,7 +361,14 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 ? 4 : 2)) combine_kerne
       if (layer == c.L) { layer = 0; ++pass; }
       const bool retire = pass >= retire_pass;
       float zv[kZJ];
-      if (!retire && c.router)
+      const T* gw = nullptr;
+      const float* gb = nullptr;
+      if (GATE && !retire) {
+        const uint64_t* ge = gate_entry(c, layer);
+        gw = reinterpret_cast<const T*>(ge[0]);
+        gb = reinterpret_cast<const float*>(ge[1]);
+      }
+      if (!retire && c.router && !gw)
         route_load(c.router + (((uint64_t)(pass % c.n_tab) * c.L + layer) * c.T + slot) * c.E, c.E, lane, zv);
       // h_new = store(h + Σ_k w_k O_k + Σ_j O_shared_j), ascending k then j, no FMA (c9);
       // shared legs use w = 1 (1·O == O exactly)
@@ -344,7 +409,13 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 ? 4 : 2)) combine_kerne
         if (lane == 0) atomicAdd(&s_retired, 1ull);
         continue;
       }
-      if (!c.router) { if (lane == 0) raise_fault(c, F_NO_ROUTER, slot, layer, pass); continue; }
+      if (GATE && gw) {
+        // the next layer's gate on the row just normalised (this warp stored x; same lanes)
+        gate_logits<T>(c, xbase + (uint64_t)slot * c.d, gw, gb, lane, zv);
+      } else if (!c.router) {
+        if (lane == 0) raise_fault(c, F_NO_ROUTER, slot, layer, pass);
+        continue;
+      }
       int my_e;
       float my_w;
       route_select(zv, c.E, c.K, lane, my_e, my_w);
@@ -395,46 +466,41 @@ int launch_enqueue(const DevCtx& c, int layer, const int32_t* slots, int n, cons
   return 1;
 }
 
-int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
-  cdrain_kernel<<<1, 32, 0, s>>>(c);
+template <typename T, int KSM, bool GATE>
+static void launch_combine_t(const DevCtx& c, int retire_pass, cudaStream_t s) {
   // persistent grid: every resident CTA slot once (no tail wave), capped by the worst case (all
   // homed tokens ready); CTAs loop over 32-token chunks of the ready list
-  const int ksm = c.KS <= 2 ? 2 : c.KS <= 4 ? 4 : c.KS <= 8 ? 8 : 12;
-  static int resident[2][4] = {{0}};
-  static int sms = 0;
-  if (!sms) {
+  static int occ = 0, sms = 0;
+  if (!occ) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int& occ = resident[c.dtype == AMOE_BF16 ? 0 : 1][ksm == 2 ? 0 : ksm == 4 ? 1 : ksm == 8 ? 2 : 3];
-#define AMOE_OCC(TT, KK) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, combine_kernel<TT, KK>, kTokThreads, 0)
-  if (!occ) {
-    if (c.dtype == AMOE_BF16) {
-      if (ksm == 2) AMOE_OCC(__nv_bfloat16, 2); else if (ksm == 4) AMOE_OCC(__nv_bfloat16, 4);
-      else if (ksm == 8) AMOE_OCC(__nv_bfloat16, 8); else AMOE_OCC(__nv_bfloat16, 12);
-    } else {
-      if (ksm == 2) AMOE_OCC(float, 2); else if (ksm == 4) AMOE_OCC(float, 4);
-      else if (ksm == 8) AMOE_OCC(float, 8); else AMOE_OCC(float, 12);
-    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, combine_kernel<T, KSM, GATE>, kTokThreads, 0);
     if (occ < 1) occ = 1;
   }
-#undef AMOE_OCC
   int grid = (c.T + kTPC - 1) / kTPC;
   if (grid > sms * occ) grid = sms * occ;
-#define AMOE_COMBINE(TT, KK) combine_kernel<TT, KK><<<grid, kTokThreads, 0, s>>>(c, retire_pass)
+  combine_kernel<T, KSM, GATE><<<grid, kTokThreads, 0, s>>>(c, retire_pass);
+}
+
+template <typename T, bool GATE>
+static void launch_combine_g(const DevCtx& c, int retire_pass, cudaStream_t s) {
+  const int ksm = c.KS <= 2 ? 2 : c.KS <= 4 ? 4 : c.KS <= 8 ? 8 : 12;
+  if (ksm == 2) launch_combine_t<T, 2, GATE>(c, retire_pass, s);
+  else if (ksm == 4) launch_combine_t<T, 4, GATE>(c, retire_pass, s);
+  else if (ksm == 8) launch_combine_t<T, 8, GATE>(c, retire_pass, s);
+  else launch_combine_t<T, 12, GATE>(c, retire_pass, s);
+}
+
+int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
+  cdrain_kernel<<<1, 32, 0, s>>>(c);
   if (c.dtype == AMOE_BF16) {
-    if (ksm == 2) AMOE_COMBINE(__nv_bfloat16, 2);
-    else if (ksm == 4) AMOE_COMBINE(__nv_bfloat16, 4);
-    else if (ksm == 8) AMOE_COMBINE(__nv_bfloat16, 8);
-    else AMOE_COMBINE(__nv_bfloat16, 12);
+    if (c.gate_on) launch_combine_g<__nv_bfloat16, true>(c, retire_pass, s);
+    else launch_combine_g<__nv_bfloat16, false>(c, retire_pass, s);
   } else {
-    if (ksm == 2) AMOE_COMBINE(float, 2);
-    else if (ksm == 4) AMOE_COMBINE(float, 4);
-    else if (ksm == 8) AMOE_COMBINE(float, 8);
-    else AMOE_COMBINE(float, 12);
+    if (c.gate_on) launch_combine_g<float, true>(c, retire_pass, s);
+    else launch_combine_g<float, false>(c, retire_pass, s);
   }
-#undef AMOE_COMBINE
   return 2;
 }
 

@@ -388,3 +388,77 @@ def test_exec_log_accounts_for_every_leg():
         assert n > 0
         per_q[l, q] += n
     assert np.array_equal(per_q, qctr[..., 2].astype(np.int64))
+
+
+def _gate_params(P, seed=31):
+    """Seeded gate weights N(0, 1/d) in storage dtype and a per-layer Zipf log-prob bias."""
+    import workload as wl
+    rng = np.random.default_rng(seed)
+    gates, dev = [], []
+    for l in range(P.L):
+        wg = (rng.standard_normal((P.E, P.d)) * P.d ** -0.5).astype(np.float32)
+        wg_store = host_values(wl.bf16_bits_from_f32(wg) if P.dtype == "bf16" else wg, P.dtype)
+        bias = np.log(wl.zipf_probs(P.E, 1.2))[wl.layer_perm(seed, l, 0, P.E).argsort()].astype(np.float32)
+        gates.append((wg_store, bias))
+        dev.append((torch.from_numpy(wg_store).to(torch.bfloat16 if P.dtype == "bf16" else torch.float32).cuda(),
+                    torch.from_numpy(bias).cuda()))
+    return gates, dev
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_gate_router_enqueue_teacher_forced(dtype):
+    """amoe_enqueue with the layer's gate: the oracle recomputes z = x·Wgᵀ + b from the GPU's own
+    x (float64) and routes it; idx must match wherever the K-th / (K+1)-th logit gap exceeds the
+    fp32 accumulation error, w within 1e-5."""
+    P = Problem(**TINY, dtype=dtype, seed=9)
+    ctx = P.make_ctx()
+    gates, dev = _gate_params(P)
+    for l in range(P.L):
+        ctx.set_gate(l, *dev[l])
+    slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
+    ctx.token_init(slots, dev_tensor(P.h0[0], dtype), 0)
+    ctx.enqueue(0, slots)                                   # no logits, no idx: the gate
+    torch.cuda.synchronize()
+    ctx.check()
+    st = ctx.state()
+    x = to_np(st["x"])
+    z = nx.gate_logits(x, *gates[0])
+    idx, w = nx.route_topk(z, P.K)
+    zs = np.sort(z.astype(np.float64), axis=1)[:, ::-1]
+    safe = (zs[:, P.K - 1] - zs[:, P.K]) > 1e-4
+    assert safe.mean() > 0.95
+    gi = st["tok_idx"].cpu().numpy()
+    gw = st["tok_w"].cpu().numpy()
+    assert np.array_equal(gi[safe], idx[safe])
+    assert np.abs(gw[safe] - w[safe]).max() <= 1e-5
+    Q = ctx.queue_depths()
+    assert Q[0].sum() == P.T * P.K
+
+
+def test_gate_router_run_matches_oracle():
+    """The full loop with every layer gate-routed (enqueue for layer 0, the combine for layer 1
+    on the freshly normalised x): final h against the oracle's synchronous run with the same
+    gates on its own x (free-running, 2 layers, bf16 gate)."""
+    P = Problem(**TINY, seed=10)
+    ctx = P.make_ctx()
+    gates, dev = _gate_params(P, seed=32)
+    for l in range(P.L):
+        ctx.set_gate(l, *dev[l])
+    slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
+    ctx.token_init(slots, dev_tensor(P.h0[0], "bf16"), 0)
+    ctx.enqueue(0, slots)
+    stats = ctx.run(retire_pass=1)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert stats["token_layers"] == P.T * P.L
+    W, SH = P.oracle_weights()
+    ref, recs = drivers.sync_run(host_values(P.h0[0], "bf16"), P.logits, W, P.K, n_passes=1, shared=SH,
+                                 gates=gates, record=True)
+    # rows whose oracle routing is not decided by an fp32-sized logit gap are compared
+    ok = np.ones(P.T, dtype=bool)
+    for r, l in zip(recs, range(P.L)):
+        zs = np.sort(nx.gate_logits(r["x"], *gates[l]).astype(np.float64), axis=1)[:, ::-1]
+        ok &= (zs[:, P.K - 1] - zs[:, P.K]) > 5e-3
+    assert ok.mean() > 0.8
+    h = to_np(ctx.state()["h"])
+    assert floored_err(h[ok], ref[ok]) <= TOL["bf16"]

@@ -229,3 +229,27 @@ def test_combine_constant_legs_return_the_leg():
     legs = np.repeat(o, 4, axis=1)
     out = nx.combine(np.zeros((50, 16), np.float32), w, legs)
     assert np.allclose(out, o[:, 0], rtol=8e-3, atol=0)
+
+
+def test_gate_logits_brute_force_and_one_hot():
+    """Router gate (f3): z = x·Wgᵀ + b. Pinned by pure-Python fsum loops on a tiny shape, by
+    one-hot gate rows (z_e = x_{j(e)} exactly) and by the bias alone (Wg = 0 -> z = b)."""
+    import math
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((5, 7)).astype(np.float32)
+    wg = rng.standard_normal((4, 7)).astype(np.float32)
+    b = rng.standard_normal(4).astype(np.float32)
+    z = nx.gate_logits(x, wg, b)
+    for t in range(5):
+        for e in range(4):
+            ref = math.fsum(float(x[t, j]) * float(wg[e, j]) for j in range(7)) + float(b[e])
+            assert abs(float(z[t, e]) - ref) <= 1e-6 * max(1.0, abs(ref))
+    onehot = np.zeros((4, 7), np.float32)
+    cols = [6, 0, 3, 3]
+    for e, j in enumerate(cols):
+        onehot[e, j] = 1.0
+    assert np.array_equal(nx.gate_logits(x, onehot), x[:, cols])
+    assert np.array_equal(nx.gate_logits(x, np.zeros((4, 7), np.float32), b), np.tile(b, (5, 1)))
+    # routing with a one-hot gate picks the largest coordinates of x among `cols`
+    idx, _ = nx.route_topk(nx.gate_logits(x, onehot), 1)
+    assert all(x[t, cols[idx[t, 0]]] == max(x[t, c] for c in cols) for t in range(5))
