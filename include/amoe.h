@@ -124,7 +124,10 @@ typedef struct amoe_run_params {
   int32_t W;           /* Algorithm 1 lookahead depth (reading c11), default 4 */
   float delta;         /* Algorithm 1 weight decay δ, default 0.5 */
   int32_t grouped;     /* 1: one launch runs every nonempty hosted queue of the picked layer */
-  int32_t max_picks;   /* safety bound on scheduler iterations; 0 = unlimited */
+  int32_t max_picks;   /* 0: run until every token retired (all ranks). > 0 (single rank):
+                          stepping mode for open-loop serving — return after this many picks or
+                          as soon as nothing is runnable; the caller admits new tokens between
+                          calls (amoe_token_init + amoe_enqueue) */
 } amoe_run_params;
 
 typedef struct amoe_run_stats {
@@ -281,7 +284,9 @@ typedef enum amoe_buffer_id {
   AMOE_BUF_RINGS = 7,     /* [L*H][ring_cap] amoe_leg */
   AMOE_BUF_QCTR = 8,      /* [L*H][4] uint32 {reserve, commit, head, pad} */
   AMOE_BUF_STATS = 9,     /* uint64 [8]: merges, retired, legs_forwarded, ... */
-  AMOE_BUF_SCRATCH = 10   /* the internal amoe_group buffers used by amoe_run (tile first) */
+  AMOE_BUF_SCRATCH = 10,  /* the internal amoe_group buffers used by amoe_run (tile first) */
+  AMOE_BUF_TOK_TIME = 11  /* [T_slots][2] uint64 device globaltimer ns: admission (amoe_token_init)
+                             and retirement (the combine that retires the token): per-token latency */
 } amoe_buffer_id;
 
 amoe_status amoe_get_buffer(amoe_ctx_t ctx, int which, void** dev_ptr, size_t* bytes);

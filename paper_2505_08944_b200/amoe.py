@@ -15,7 +15,8 @@ MAX_G, MAX_E, MAX_GROUP = 8, 256, 128
 BF16, FP32 = 0, 1
 DEFRAG, MTFS, FLFS, SYNC = 0, 1, 2, 3
 POLICIES = {"defrag": DEFRAG, "mtfs": MTFS, "flfs": FLFS, "sync": SYNC}
-BUF = dict(h=0, x=1, pool=2, tok_w=3, tok_idx=4, tok_layer=5, tok_pass=6, rings=7, qctr=8, stats=9, scratch=10)
+BUF = dict(h=0, x=1, pool=2, tok_w=3, tok_idx=4, tok_layer=5, tok_pass=6, rings=7, qctr=8, stats=9, scratch=10,
+           tok_time=11)
 STATUS = {0: "OK", 1: "IDLE", 2: "EINVAL", 3: "ENOTHOSTED", 4: "ECUDA", 5: "EDEVICE", 6: "EPEER", 7: "ENOMEM"}
 FAULTS = {1: "ring overflow", 2: "leg count > K+S", 3: "expert index out of range", 4: "not hosted",
           5: "combine ring overflow", 6: "token slot out of range", 7: "stale/unpublished ring entry",
@@ -374,6 +375,7 @@ class Context:
             tok_pass=self.buffer("tok_pass", torch.int32, (self.T,)),
             qctr=self.buffer("qctr", torch.int32, (self.L, self.H, 4)),
             stats=self.buffer("stats", torch.int64, (8,)),
+            tok_time=self.buffer("tok_time", torch.int64, (self.T, 2)),
         )
 
     def ring(self, layer, local_q):

@@ -49,6 +49,7 @@ struct Layout {
   uint64_t tok_pass;   // i32[T]
   uint64_t tok_w;      // f32[T][K]
   uint64_t tok_idx;    // i32[T][K]
+  uint64_t tok_time;   // u64[T][2]: globaltimer (ns) at admission (token_init) and at retirement
   uint64_t wmaps;      // CUtensorMap[L*H][3]
   uint64_t wptrs;      // u64[L*H][3]
   uint64_t gate;       // u64[L][2]: router gate weights [E][d] (storage dtype) and bias [E] fp32, or 0
@@ -243,6 +244,12 @@ template <> struct Vec<float> {
     f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y); f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
   }
 };
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -191,6 +191,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->tok_pass = take(T * 4);
   L->tok_w = take(T * c->K * 4);
   L->tok_idx = take(T * c->K * 4);
+  L->tok_time = take(T * 16, 16);
   L->wmaps = take((uint64_t)c->L * H * 3 * 128, 128);
   L->wptrs = take((uint64_t)c->L * H * 3 * 8);
   L->gate = take((uint64_t)c->L * 16);
@@ -642,6 +643,7 @@ amoe_status amoe_get_buffer(amoe_ctx_t c, int which, void** ptr, size_t* bytes) 
     case AMOE_BUF_QCTR: off = c->lay.qctr; n = (uint64_t)c->cfg.L * c->H * 16; break;
     case AMOE_BUF_STATS: off = c->lay.stats; n = 64; break;
     case AMOE_BUF_SCRATCH: off = c->lay.s_tile; n = c->lay.total - c->lay.s_tile; break;
+    case AMOE_BUF_TOK_TIME: off = c->lay.tok_time; n = T * 16; break;
     default: return AMOE_EINVAL;
   }
   *ptr = c->ws + off;
@@ -694,6 +696,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
     rs.wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t_run0).count();
     if (out) *out = rs;
   };
+  // stepping mode (max_picks > 0, single rank): return after max_picks picks or as soon as
+  // nothing is runnable — the caller admits arrivals in between (open-loop serving); no
+  // quiescence protocol, no lost-leg verdict
+  const bool stepping = p->max_picks > 0;
+  if (stepping && c->cfg.G > 1) return AMOE_EINVAL;
   for (;;) {
     const auto t_poll = clk::now();
     st = snapshot(c, s);
@@ -702,7 +709,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
     if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return AMOE_EDEVICE;
     const uint64_t* sv = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
     log_executions(c, false);
-    if (sync && !announced) {
+    if (sync && !announced && !stepping) {
       const uint32_t* flags = reinterpret_cast<const uint32_t*>(snap + c->lay.done) + AMOE_MAX_G;
       if (!sync_arrived && (int64_t)(sv[0] - merged0) >= expected * (int64_t)(rs.barriers + 1) &&
           (int64_t)(sv[1] - retired0) < expected) {   // the last layer of the run has no barrier
@@ -726,7 +733,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         }
       }
     }
-    if (!announced && (int64_t)(sv[1] - retired0) >= expected) {
+    if (!stepping && !announced && (int64_t)(sv[1] - retired0) >= expected) {
       c->launches += launch_announce(c->dc, epoch, 0, s);
       rs.kernel_launches += 1;
       announced = true;
@@ -785,6 +792,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       idle_streak = 0;
     } else {
       rs.idle_polls += 1;
+      if (stepping) {
+        rs.token_layers = (int64_t)(sv[0] - merged0);
+        rs.legs = (int64_t)(sv[2] - legs0);
+        break;
+      }
       if (c->cfg.G == 1 && !announced && !sync_arrived) {
         // single GPU: nothing queued and tokens not retired means a lost leg
         rs.token_layers = (int64_t)(sv[0] - merged0);
@@ -794,7 +806,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       if (++idle_streak > 64) std::this_thread::sleep_for(std::chrono::microseconds(5));
       rs.idle_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t_poll).count();
     }
-    if (p->max_picks > 0 && rs.picks >= p->max_picks) break;
+    if (stepping && rs.picks >= p->max_picks) {
+      rs.token_layers = (int64_t)(sv[0] - merged0);   // merges observed up to this pick's launch
+      rs.legs = (int64_t)(sv[2] - legs0);
+      break;
+    }
   }
   finish(stats);
   return AMOE_OK;

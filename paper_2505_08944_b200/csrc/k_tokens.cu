@@ -226,6 +226,9 @@ __global__ void __launch_bounds__(kTokThreads) token_init_kernel(DevCtx c, const
     ss = warp_sum(ss);
     rmsnorm_row<T>(c, h, x, ss, lane);
     if (lane == 0) {
+      unsigned long long* tt = wsp<unsigned long long>(c, c.rank, c.lay.tok_time) + 2 * (uint64_t)slot;
+      tt[0] = globaltimer_ns();
+      tt[1] = 0;
       wsp<int32_t>(c, c.rank, c.lay.tok_layer)[slot] = 0;
       wsp<int32_t>(c, c.rank, c.lay.tok_pass)[slot] = pass;
       wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
@@ -406,7 +409,10 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
       rmsnorm_row<T>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);
       if (lane == 0) { tlayer[slot] = layer; tpass[slot] = pass; atomicAdd(&s_merged, 1ull); }
       if (retire) {
-        if (lane == 0) atomicAdd(&s_retired, 1ull);
+        if (lane == 0) {
+          atomicAdd(&s_retired, 1ull);
+          wsp<unsigned long long>(c, c.rank, c.lay.tok_time)[2 * (uint64_t)slot + 1] = globaltimer_ns();
+        }
         continue;
       }
       if (GATE && gw) {

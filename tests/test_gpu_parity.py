@@ -462,3 +462,39 @@ def test_gate_router_run_matches_oracle():
     assert ok.mean() > 0.8
     h = to_np(ctx.state()["h"])
     assert floored_err(h[ok], ref[ok]) <= TOL["bf16"]
+
+
+def test_open_loop_stepping_and_token_times():
+    """Stepping mode (max_picks > 0) for open-loop serving: tokens admitted in three waves between
+    single-pick calls retire exactly once each, with the same h as one closed-loop run (every
+    row's arithmetic is batch-independent), and every token has admission < retirement times."""
+    P = Problem(**TINY, seed=12)
+    ref_ctx = P.make_ctx()
+    admit(ref_ctx, P)
+    ref_ctx.run(retire_pass=1)
+    torch.cuda.synchronize()
+    ref = to_np(ref_ctx.state()["h"])
+    ctx = P.make_ctx()
+    h0 = dev_tensor(P.h0[0], "bf16")
+    z0 = torch.from_numpy(np.ascontiguousarray(P.tables[0][0, 0])).cuda()
+    cuts = [0, 100, 300, P.T]
+    picks = 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sl = torch.arange(a, b, dtype=torch.int32, device="cuda")
+        ctx.token_init(sl, h0[a:b].contiguous(), 0)
+        ctx.enqueue(0, sl, logits=z0[a:b].contiguous())
+        st = ctx.run(retire_pass=1, max_picks=1)
+        picks += st["picks"]
+    for _ in range(1000):
+        st = ctx.run(retire_pass=1, max_picks=1)
+        picks += st["picks"]
+        if st["picks"] == 0 and int(ctx.state()["stats"][1]) == P.T:
+            break
+    torch.cuda.synchronize()
+    ctx.check()
+    s = ctx.state()
+    assert int(s["stats"][1]) == P.T and int(s["stats"][0]) == P.T * P.L
+    assert np.array_equal(to_np(s["h"]), ref)
+    tt = s["tok_time"].cpu().numpy()
+    assert np.all(tt[:, 0] > 0) and np.all(tt[:, 1] > tt[:, 0])
+    assert picks >= P.L
