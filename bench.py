@@ -391,6 +391,7 @@ def main():
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
         "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router),
         "gpu_launches": int(launches),
+        "die_map_sms": list(amoe.die_info()),
         "clocks": clk,
         "stall": {"idle_frac_per_rank": [round(v[0], 4) for v in stall], "layer_barriers": int(stall[0][1]),
                   "definition": "time a rank's scheduler found no runnable queue / its amoe_run wall time"},

@@ -91,6 +91,7 @@ EXPORTS = {
     "amoe_local_queue": (C.c_int, [C.c_void_p, C.c_int]),
     "amoe_scratch_group": (C.c_int, [C.c_void_p, C.POINTER(Group)]),
     "amoe_launch_count": (C.c_int64, [C.c_void_p]),
+    "amoe_die_info": (C.c_int, [C.POINTER(C.c_int32)]),
     "amoe_check": (C.c_int, [C.c_void_p]),
     "amoe_error_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32)]),
     "amoe_clear_error": (C.c_int, [C.c_void_p]),
@@ -150,6 +151,15 @@ def make_config(L, E, K, S, d, ff, T_slots, G=1, rank=0, dtype="bf16", max_batch
 
 def workspace_bytes(cfg: Config) -> int:
     return int(load().amoe_workspace_bytes(C.byref(cfg)))
+
+
+def die_info():
+    """(SMs on die 0, SMs on die 1) from the library's probe; (n, 0) = no die split detected."""
+    c = (C.c_int32 * 2)()
+    st = load().amoe_die_info(c)
+    if st != 0:
+        raise AmoeError(st, "amoe_die_info")
+    return int(c[0]), int(c[1])
 
 
 def schedule(Q, n_experts, policy="defrag", W=4, delta=0.5):

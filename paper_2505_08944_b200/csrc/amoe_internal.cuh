@@ -41,6 +41,7 @@ struct Layout {
   uint64_t cctr;       // u32[4]: combine ring reserve, commit, head, pad
   uint64_t cring;      // amoe_leg[cring_cap]
   uint64_t cinfo;      // i32[4]: combine drain n, start
+  uint64_t sched;      // u32[4]: FFN die-aware tile claims {die 0, die 1, finished clusters, pad}
   uint64_t split_cnt;  // u32[kSplitSlots]: split-K arrival counters (self-resetting)
   uint64_t h, x;       // [T][d]
   uint64_t pool;       // [T][K+S][d]
@@ -68,7 +69,9 @@ struct DevCtx {
   int32_t n_tab;
   const float* router;               // local [n_tab][L][T][E] or null
   int32_t gate_on;                   // some layer has a router gate (amoe_set_gate)
-  int32_t pad_gate;
+  int32_t die_cnt[2];                // SMs on each die (die_probe); die_cnt[1] == 0: no die split
+  int32_t pad_die;
+  uint64_t die_mask[4];              // bit smid set: SM on die 1
   Layout lay;
   uint64_t peer[AMOE_MAX_G];         // workspace base per rank; peer[rank] = local
   int16_t lq[AMOE_MAX_E];            // local queue index of routed expert e on its owner

@@ -18,6 +18,7 @@ int launch_token_init(const DevCtx&, const int32_t*, int, const void*, int, cuda
 int launch_enqueue(const DevCtx&, int, const int32_t*, int, const float*, const int32_t*, const float*, cudaStream_t);
 int launch_combine(const DevCtx&, int, cudaStream_t);
 int launch_announce(const DevCtx&, uint32_t, int, cudaStream_t);
+int die_map(uint64_t mask[4], int counts[2]);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
@@ -182,6 +183,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->rings = take((uint64_t)c->L * H * rc * 16);
   L->cring = take((uint64_t)crc * 16);
   L->cinfo = take(16);
+  L->sched = take(16);
   L->split_cnt = take((uint64_t)kSplitSlots * 4);
   L->h = take(T * d * es);
   L->x = take(T * d * es);
@@ -259,6 +261,7 @@ amoe_status amoe_create(const amoe_config* cfg, void* workspace, size_t bytes, a
   d.ring_cap = rc; d.ring_mask = rc - 1; d.cring_cap = crc; d.cring_mask = crc - 1;
   d.eps = cfg->rms_eps > 0.f ? cfg->rms_eps : 1e-6f;
   d.n_tab = 0; d.router = nullptr;
+  die_map(d.die_mask, d.die_cnt);     // cached per device after the first context
   d.lay = c->lay;
   int owner[AMOE_MAX_E];
   resolve_owner(cfg, owner);

@@ -14,6 +14,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "amoe_internal.cuh"
 
@@ -52,6 +53,8 @@ struct FfnArgs {
   int32_t gather;        // GATEUP: 1 = A rows gathered from x by token slot (TMA tile::gather4)
   int32_t allow_split;   // split K when the output tiles cannot fill the machine (cold experts)
   int32_t atrim;         // partial M tiles load only their valid A rows
+  int32_t die_sched;     // CTA-pair kernels: die-aware dynamic tile claims (unit ring)
+  uint32_t* sched;       // u32[4] claim counters {die 0, die 1, finished clusters} (self-resetting)
   float* part;           // split-K fp32 partials (workspace)
   uint32_t* cnt;         // split-K per-slot arrival counters (workspace, self-resetting)
   const amoe_leg* meta;  // [rows] drained legs (fused forward) when !ring_legs
@@ -651,6 +654,34 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(bar_cluster) : "memory");
 }
 
+// ------------------------------------------------------------------ die-aware unit ring
+// The leader's producer claims units (tile, K split) from its die's list — each die owns a
+// share of every queue's N tiles, so a weight slab is streamed into one die's L2 only —
+// stealing from the other die's list when its own runs out, and publishes each unit to a ring
+// in both CTAs' shared memory. The leader's MMA issuer and epilogue and the peer's producer
+// and epilogue consume the ring in order (4 arrivals free a slot).
+constexpr int RING = 8;
+__device__ __forceinline__ uint32_t smid_u32() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAITC_%=;\n}\n" :: "r"(bar), "r"(parity), "r"(kSuspendNs) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, int4 v) {
+  asm volatile("st.shared::cluster.v4.s32 [%0], {%1, %2, %3, %4};"
+               :: "r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
 struct Sched2 {
   int nq, n_tiles, total, group;
   const int* n;
@@ -675,6 +706,7 @@ template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
   __shared__ unsigned long long s_fwd[2];
+  __shared__ int4 s_epi_rec[1];            // die schedule: the epilogue's current unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
@@ -685,6 +717,13 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   int* s_off = s_n + AMOE_MAX_GROUP;
   int* s_pre = s_off + AMOE_MAX_GROUP;
   int* s_start = s_pre + AMOE_MAX_GROUP + 1;
+  // die-aware schedule: per-die tile prefix sums, the unit ring and its barriers
+  int* s_pre_d = s_start + AMOE_MAX_GROUP + 4;                       // [2][AMOE_MAX_GROUP + 1]
+  int4* ring = reinterpret_cast<int4*>(((reinterpret_cast<uintptr_t>(s_pre_d + 2 * (AMOE_MAX_GROUP + 1))) + 15) &
+                                       ~uintptr_t(15));
+  uint64_t* ring_full = reinterpret_cast<uint64_t*>(ring + RING);
+  uint64_t* ring_empty = ring_full + RING;
+  int* s_die = reinterpret_cast<int*>(ring_empty + RING);           // [0] = N-tile split point
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = cluster_rank();
@@ -711,6 +750,19 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
       mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 2);     // one arrive per CTA of the pair
     }
+    if (args.die_sched) {
+      // die d owns N tiles [lo_d, hi_d) of every queue, in proportion to its SM count
+      const int tot = dc.die_cnt[0] + dc.die_cnt[1];
+      const int h = (args.n_tiles * dc.die_cnt[0] + tot / 2) / tot;
+      s_die[0] = h;
+      for (int d = 0; d < 2; ++d) {
+        const int nbd = d == 0 ? h : args.n_tiles - h;
+        int a2 = 0;
+        for (int q = 0; q < nq; ++q) { s_pre_d[d * (AMOE_MAX_GROUP + 1) + q] = a2; a2 += (s_n[q] + BM2 - 1) / BM2 * nbd; }
+        s_pre_d[d * (AMOE_MAX_GROUP + 1) + nq] = a2;
+      }
+      for (int r = 0; r < RING; ++r) { mbar_init(smem_u32(&ring_full[r]), 1); mbar_init(smem_u32(&ring_empty[r]), 4); }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&tmA);
   }
@@ -728,16 +780,109 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int split = choose_split(args, sc.total, ncl, 2, s_start[AMOE_MAX_GROUP], s_start[AMOE_MAX_GROUP + 1]);
   const int units = sc.total * split;
+  const bool die_sched = args.die_sched != 0;
+  // unit = {q, m, nb, ks}; q < 0: no more units. Static schedule: cluster cl takes units
+  // cl, cl + ncl, ... of the global raster.
+  auto static_unit = [&](int it) -> int4 {
+    const int u = cl + it * ncl;
+    if (u >= units) return make_int4(-1, 0, 0, 0);
+    const int t = u / split;
+    int q, m, nb;
+    sc.decode(t, q, m, nb);
+    return make_int4(q, m, nb, u - t * split);
+  };
+  // die-local unit u of die d -> {q, m, nb, ks}: the raster of Sched2 restricted to the die's
+  // N tiles [lo_d, hi_d) of every queue (measured: contiguous ranges of whole queues per die
+  // kept the DRAM traffic; this split cut the Mixtral gate/up reads 5.6 -> 3.4 GB)
+  auto die_units = [&](int d) -> int { return s_pre_d[d * (AMOE_MAX_GROUP + 1) + nq] * split; };
+  auto die_unit = [&](int d, int u) -> int4 {
+    const int* pre = s_pre_d + d * (AMOE_MAX_GROUP + 1);
+    const int lo = d == 0 ? 0 : s_die[0];
+    const int nbd = d == 0 ? s_die[0] : args.n_tiles - s_die[0];
+    const int t = u / split;
+    int qlo = 0, qhi = nq - 1;
+    while (qlo < qhi) { const int mid = (qlo + qhi + 1) >> 1; if (pre[mid] <= t) qlo = mid; else qhi = mid - 1; }
+    const int q = qlo;
+    const int r = t - pre[q];
+    const int m_tiles = (s_n[q] + BM2 - 1) / BM2;
+    const int gsz = sc.group * nbd;
+    const int g = r / gsz;
+    const int first_m = g * sc.group;
+    const int gm = min(m_tiles - first_m, sc.group);
+    const int rr = r - g * gsz;
+    return make_int4(q, first_m + rr % gm, lo + rr / gm, u - t * split);
+  };
+  // leader producer: claims are issued one unit ahead (the atomic's latency overlaps the
+  // current unit's loads) and resolved — own die first, then the other die's list — into the
+  // unit published to both CTAs' rings one unit ahead of its loads
+  const int my_die = (int)((dc.die_mask[smid_u32() >> 6] >> (smid_u32() & 63)) & 1ull);
+  int claim_d = my_die;
+  uint32_t claim_u = 0;
+  auto issue_claim = [&]() { claim_u = atomicAdd(args.sched + claim_d, 1u); };
+  auto resolve_claim = [&]() -> int4 {
+    for (;;) {
+      const int ud = die_units(claim_d);
+      if (claim_u < (uint32_t)ud) return die_unit(claim_d, (int)claim_u);
+      if (claim_d != my_die) return make_int4(-1, 0, 0, 0);     // both lists exhausted
+      claim_d = 1 - my_die;                                     // steal
+      issue_claim();
+    }
+  };
+  auto publish = [&](int it, int4 rec) {
+    const int slot = it % RING;
+    mbar_wait_cluster(smem_u32(&ring_empty[slot]), ((it / RING) & 1) ^ 1u);
+    const uint32_t a_loc = smem_u32(&ring[slot]);
+    st_cluster_v4(mapa(a_loc, 0), rec);
+    st_cluster_v4(mapa(a_loc, 1), rec);
+    mbar_arrive_cluster(mapa(smem_u32(&ring_full[slot]), 0));
+    mbar_arrive_cluster(mapa(smem_u32(&ring_full[slot]), 1));
+  };
+  int4 next_unit = make_int4(-1, 0, 0, 0);
+  auto claim_publish = [&](int it) -> int4 {
+    if (it == 0) {                         // unit 0 now; the claim for unit 1 in flight
+      issue_claim();
+      next_unit = resolve_claim();
+      publish(0, next_unit);
+      if (next_unit.x >= 0) issue_claim();
+    }
+    const int4 cur = next_unit;            // published one unit ago
+    if (cur.x >= 0) {
+      next_unit = resolve_claim();
+      publish(it + 1, next_unit);
+      if (next_unit.x >= 0) issue_claim();
+    }
+    return cur;
+  };
+  // every other role (one thread): take unit `it` from this CTA's ring, free the slot. The free
+  // is a relaxed arrive ordered after the record load by a dependency on its value: a release
+  // arrive would first drain this thread's outstanding global stores (the epilogue's output
+  // rows), stalling the epilogue for microseconds per unit.
+  auto ring_get = [&](int it) -> int4 {
+    const int slot = it % RING;
+    mbar_wait_cluster(smem_u32(&ring_full[slot]), (it / RING) & 1);
+    const int4 rec = lds_v4(smem_u32(&ring[slot]));
+    // (rec.x is a queue index or -1, never INT_MIN: the select is 0, but the address depends on
+    // the loaded value, so the arrive cannot be performed before the load)
+    const uint32_t eb = mapa(smem_u32(&ring_empty[slot]), 0) + (rec.x == INT_MIN ? 8u : 0u);
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" :: "r"(eb) : "memory");
+    return rec;
+  };
 
   if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
     // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
     // the leader's full barrier (whole warp when A rows are gathered: lane i -> rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
-    for (int u = cl; u < units; u += ncl) {
-      const int t = u / split, ks = u - t * split;
+    const bool gw = MODE == MODE_GATEUP && args.gather;     // whole warp in this branch
+    for (int it = 0;; ++it) {
+      int4 U = make_int4(-1, 0, 0, 0);
+      if (lane == 0) U = !die_sched ? static_unit(it) : leader ? claim_publish(it) : ring_get(it);
+      if (gw) {
+        U.x = __shfl_sync(0xffffffffu, U.x, 0); U.y = __shfl_sync(0xffffffffu, U.y, 0);
+        U.z = __shfl_sync(0xffffffffu, U.z, 0); U.w = __shfl_sync(0xffffffffu, U.w, 0);
+      }
+      if (U.x < 0) break;
+      const int q = U.x, m = U.y, nb = U.z, ks = U.w;
       const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
-      int q, m, nb;
-      sc.decode(t, q, m, nb);
       const int arow = s_off[q] + m * BM2 + (int)crank * 128;
       const CUtensorMap* wb = args.wmaps + args.wslot[q] + args.w_which;
       const CUtensorMap* bmap = (MODE == MODE_GATEUP) ? wb + crank : wb;
@@ -777,8 +922,10 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     constexpr uint32_t idesc = idesc_bf16(BM2, 256);
     int stage = 0; uint32_t phase = 0;
     int acc = 0; uint32_t acc_phase = 0;
-    for (int u = cl; u < units; u += ncl) {
-      const int ks = u % split;
+    for (int it = 0;; ++it) {
+      const int4 U = die_sched ? ring_get(it) : static_unit(it);
+      if (U.x < 0) break;
+      const int ks = U.w;
       const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
       mbar_wait(smem_u32(&bars[2 * STAGES2 + 2 + acc]), acc_phase ^ 1u);
       tc_fence_after();
@@ -805,10 +952,18 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     uint32_t fwd[2] = {0u, 0u};
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&bars[2 * STAGES2 + 2]), 0);
-    for (int u = cl; u < units; u += ncl) {
-      const int t = u / split, ks = u - t * split;
-      int q, m, nb;
-      sc.decode(t, q, m, nb);
+    for (int it = 0;; ++it) {
+      int4 U;
+      if (die_sched) {
+        if (tid == 128) s_epi_rec[0] = ring_get(it);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        U = s_epi_rec[0];
+      } else {
+        U = static_unit(it);
+      }
+      if (U.x < 0) break;
+      const int q = U.x, m = U.y, nb = U.z, ks = U.w;
+      const int t = s_pre[q] + nb;           // split units: the tile's global index (m = 0)
       epi_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase, tid, 128);
       tc_fence_after();
       const int row = m * BM2 + (int)crank * 128 + ew * 32 + lane;
@@ -833,6 +988,14 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
         fwd[1] += __shfl_xor_sync(0xffffffffu, fwd[1], o);
       }
       if (lane == 0) { atomicAdd(&s_fwd[0], (unsigned long long)fwd[0]); atomicAdd(&s_fwd[1], (unsigned long long)fwd[1]); }
+    }
+  }
+  if (die_sched && leader && tid == 0) {
+    // every cluster has claimed its last unit before it gets here; the last one resets the
+    // claim counters for the next launch (stream-ordered)
+    if (atomicAdd(args.sched + 2, 1u) == (uint32_t)(ncl - 1)) {
+      args.sched[0] = 0; args.sched[1] = 0; args.sched[2] = 0;
+      __threadfence();
     }
   }
   tc_fence_before();
@@ -988,6 +1151,141 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, 
 // ------------------------------------------------------------------ launchers
 
 
+// ================================================================== SM -> die map
+// B200 is two dies; each die's L2 caches its own half of the address space (2 KB interleave),
+// and an SM reaches the other die's L2 over the die-to-die fabric (measured here: 28-cycle
+// longer hits; tools/die_probe.cu). One CTA per SM times dependent L2 hits to NL lines; SMs of
+// one die agree on which lines are near. The map is yield-dependent, so it is measured at run
+// time (once per device) and used to give each die's CTA pairs their own share of the weight
+// slabs (die-aware FFN schedule).
+namespace probe {
+constexpr int NL = 128;
+constexpr int REP = 16;
+__global__ void die_probe_kernel(const uint32_t* buf, uint32_t* lat, int* smids) {
+  if (threadIdx.x != 0) return;
+  int sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  smids[blockIdx.x] = sm;
+  const uint32_t zero = buf[NL * 512 + 7];
+  uint32_t v = 0;
+  for (int i = 0; i < NL; ++i) {          // warm: every line into L2
+    uint32_t w;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(w) : "l"(buf + i * 512) : "memory");
+    v |= w;
+  }
+  for (int i = 0; i < NL; ++i) {
+    const uint32_t* base = buf + i * 512;
+    uint64_t t0, t1;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0) :: "memory");
+    for (int r = 0; r < REP; ++r)
+      asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(base + (v & zero)) : "memory");
+    asm volatile("{\n.reg .u64 t;\nmov.u64 t, %%clock64;\nadd.u64 %0, t, %1;\n}"
+                 : "=l"(t1) : "l"((uint64_t)(v & zero)) : "memory");
+    lat[blockIdx.x * NL + i] = (uint32_t)((t1 - t0) / REP);
+  }
+}
+}  // namespace probe
+
+int die_map(uint64_t mask[4], int counts[2]);
+}  // namespace amoe
+
+extern "C" amoe_status amoe_die_info(int32_t counts[2]) {
+  if (!counts) return AMOE_EINVAL;
+  uint64_t mask[4];
+  int c[2];
+  amoe::die_map(mask, c);
+  counts[0] = c[0];
+  counts[1] = c[1];
+  return AMOE_OK;
+}
+
+namespace amoe {
+int die_map(uint64_t mask[4], int counts[2]) {
+  static int cached_dev = -1;
+  static uint64_t c_mask[4];
+  static int c_cnt[2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cached_dev != dev) {
+    c_mask[0] = c_mask[1] = c_mask[2] = c_mask[3] = 0;
+    c_cnt[0] = c_cnt[1] = 0;
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    c_cnt[0] = nsm;
+    const char* env = getenv("AMOE_DIE_SCHED");
+    uint32_t *buf = nullptr, *lat = nullptr;
+    int* sms = nullptr;
+    bool ok = (!env || env[0] != '0') && nsm <= 256 &&
+              cudaMalloc(&buf, probe::NL * 2048 + 4096) == cudaSuccess &&
+              cudaMalloc(&lat, (size_t)nsm * probe::NL * 4) == cudaSuccess &&
+              cudaMalloc(&sms, (size_t)nsm * 4) == cudaSuccess &&
+              cudaMemset(buf, 0, probe::NL * 2048 + 4096) == cudaSuccess &&
+              cudaFuncSetAttribute(probe::die_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024) == cudaSuccess;
+    std::vector<uint32_t> L((size_t)nsm * probe::NL);
+    std::vector<int> S(nsm);
+    if (ok) {
+      probe::die_probe_kernel<<<nsm, 32, 200 * 1024>>>(buf, lat, sms);    // one CTA per SM
+      ok = cudaDeviceSynchronize() == cudaSuccess &&
+           cudaMemcpy(L.data(), lat, L.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+           cudaMemcpy(S.data(), sms, S.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    }
+    if (buf) cudaFree(buf);
+    if (lat) cudaFree(lat);
+    if (sms) cudaFree(sms);
+    cudaGetLastError();
+    if (ok) {
+      // per SM: which lines are near (below the midpoint of its own min / max); SMs are then
+      // split by agreement with SM 0's pattern, refined once against each group's majority
+      const int NLn = probe::NL;
+      std::vector<std::vector<char>> near(nsm, std::vector<char>(NLn));
+      for (int b = 0; b < nsm; ++b) {
+        uint32_t lo = ~0u, hi = 0;
+        for (int i = 0; i < NLn; ++i) { lo = std::min(lo, L[b * NLn + i]); hi = std::max(hi, L[b * NLn + i]); }
+        for (int i = 0; i < NLn; ++i) near[b][i] = 2 * L[b * NLn + i] < lo + hi;
+      }
+      std::vector<int> grp(nsm);
+      for (int b = 0; b < nsm; ++b) {
+        int agree = 0;
+        for (int i = 0; i < NLn; ++i) agree += near[b][i] == near[0][i];
+        grp[b] = agree >= NLn / 2 ? 0 : 1;
+      }
+      std::vector<char> cons(NLn);                      // group 0's majority pattern
+      for (int i = 0; i < NLn; ++i) {
+        int v = 0, n = 0;
+        for (int b = 0; b < nsm; ++b)
+          if (grp[b] == 0) { v += near[b][i]; ++n; }
+        cons[i] = 2 * v >= n;
+      }
+      int cnt[2] = {0, 0};
+      uint64_t m[4] = {0, 0, 0, 0};
+      bool clean = true;
+      std::vector<char> seen(256, 0);
+      for (int b = 0; b < nsm; ++b) {
+        int agree = 0;
+        for (int i = 0; i < NLn; ++i) agree += near[b][i] == cons[i];
+        if (10 * agree > 3 * NLn && 10 * agree < 7 * NLn) clean = false;   // ambiguous SM
+        const int die = 2 * agree >= NLn ? 0 : 1;
+        const int smid = S[b];
+        if (smid < 0 || smid >= 256 || seen[smid]) { clean = false; continue; }
+        seen[smid] = 1;
+        cnt[die] += 1;
+        if (die) m[smid >> 6] |= 1ull << (smid & 63);
+      }
+      if (clean && cnt[0] >= nsm / 4 && cnt[1] >= nsm / 4) {
+        for (int i = 0; i < 4; ++i) c_mask[i] = m[i];
+        c_cnt[0] = cnt[0];
+        c_cnt[1] = cnt[1];
+      }
+    }
+    cached_dev = dev;
+  }
+  for (int i = 0; i < 4; ++i) mask[i] = c_mask[i];
+  counts[0] = c_cnt[0];
+  counts[1] = c_cnt[1];
+  return c_cnt[1] > 0;
+}
+
 // part 1: gate/up + SwiGLU -> act; part 2: down -> out, or (fuse) straight into the home pools.
 // gathered: A rows of part 1 come from x by token slot (tm_tile is then the x map, box {64, 1})
 // and both parts read the drained legs from the rings (no gather kernel, no meta copy).
@@ -1015,7 +1313,8 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.cnt = reinterpret_cast<uint32_t*>(c.peer[c.rank] + c.lay.split_cnt);
   const char* es = getenv("AMOE_SPLITK");
   a.allow_split = es ? (es[0] == '1') : 1;
-  const char* et = getenv("AMOE_ATRIM");
+  a.sched = reinterpret_cast<uint32_t*>(c.peer[c.rank] + c.lay.sched);
+    const char* et = getenv("AMOE_ATRIM");
   a.atrim = et ? (et[0] == '1') : 1;
   a.ring_legs = gathered;
   a.gather = (part == 1) ? gathered : 0;
@@ -1047,6 +1346,12 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     a.out = reinterpret_cast<__nv_bfloat16*>(out);
     a.fuse = fuse;
   }
+  // die-aware claims where weight slabs are long (K >= 4096: Mixtral-shaped GEMMs, where the
+  // split halves the slab traffic); short-K GEMMs (DeepSeek-shaped) measured faster static
+  // (AMOE_DIE_SCHED: 0 = never, 2 = every CTA-pair GEMM; read per launch, for A/B and tests)
+  const char* ed = getenv("AMOE_DIE_SCHED");
+  const int dmode = ed ? atoi(ed) : 1;
+  a.die_sched = c.die_cnt[1] > 0 && dmode != 0 && (dmode == 2 || a.k_blocks >= 64) ? 1 : 0;
   if (pair) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(num_sms & ~1));

@@ -241,3 +241,37 @@ def test_mixtral_layer_fullsize_sampled():
     ref_h = nx.combine(h_before, w_gpu, to_np(st["pool"]), None, "bf16")
     assert np.array_equal(to_np(st["h"]), ref_h)
     assert int(st["stats"][1]) == P.T                          # L = 1: every token retired
+
+
+@pytest.mark.parametrize("d,ff,T,S", [(256, 512, 700, 0), (2048, 1408, 2048, 2)])
+def test_die_aware_schedule_equals_static(d, ff, T, S):
+    """The die-aware dynamic tile schedule of the CTA-pair kernels (units claimed per die from
+    each die's share of the N tiles, published through a shared-memory ring) computes every tile
+    with the same arithmetic as the static raster: bit-identical outputs, every token merged
+    once. AMOE_DIE_SCHED=2 forces it on every GEMM, 0 turns it off (read per launch)."""
+    import os
+    from paper_2505_08944_b200 import amoe
+    if amoe.die_info()[1] == 0:
+        pytest.skip("no die split detected on this device")
+    outs = []
+    old = os.environ.get("AMOE_DIE_SCHED")
+    try:
+        for mode in ("2", "0", "2"):
+            os.environ["AMOE_DIE_SCHED"] = mode
+            P = Problem(L=2, E=8, K=2, S=S, d=d, ff=ff, T=T, seed=23)
+            ctx = P.make_ctx()
+            slots = torch.arange(T, dtype=torch.int32, device="cuda")
+            ctx.token_init(slots, dev_tensor(P.h0[0], "bf16"), 0)
+            ctx.enqueue(0, slots, logits=torch.from_numpy(np.ascontiguousarray(P.tables[0][0, 0])).cuda())
+            st = ctx.run(retire_pass=1)
+            torch.cuda.synchronize()
+            ctx.check()
+            assert st["token_layers"] == T * 2
+            outs.append(to_np(ctx.state()["h"]))
+            ctx.close()
+    finally:
+        if old is None:
+            os.environ.pop("AMOE_DIE_SCHED", None)
+        else:
+            os.environ["AMOE_DIE_SCHED"] = old
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
