@@ -295,6 +295,28 @@ __device__ __forceinline__ void store_rows_staged(const uint32_t (&w)[NW], __nv_
   }
 }
 
+// Fused forward (a7) leg counting, one unit behind the stores: the row's pieces of a tile are
+// counted on the token's leg counter only at the next tile's epilogue (or at the kernel's end),
+// after a fence that by then finds those stores long completed — so the epilogue never waits
+// for its own output stores to drain (ncu: the per-tile fence was the down GEMM epilogue's top
+// stall on DeepSeek-shaped layers).
+struct PendCount {
+  amoe_leg leg;
+  int32_t pieces;   // 0: nothing pending for this lane's row
+  int32_t nb;
+};
+__device__ __forceinline__ void flush_count(const DevCtx& dc, PendCount& pend, uint32_t (&fwd)[2]) {
+  if (!__any_sync(0xffffffffu, pend.pieces > 0)) return;
+  // every lane orders its own (staged) stores, then the row's owner lane counts the pieces
+  fence_sc(dc.G > 1);
+  __syncwarp();
+  if (pend.pieces > 0) {
+    leg_pieces_done(dc, pend.leg.home, pend.leg.token_slot, pend.leg.k, (uint32_t)pend.pieces);
+    if (pend.nb == 0) { fwd[0] += 1; fwd[1] += (pend.leg.home != dc.rank); }
+  }
+  pend.pieces = 0;
+}
+
 // Non-split epilogue of one tile: every TMEM column this thread needs is loaded (and packed to
 // bf16) first, the accumulator is released to the MMA issuer, and only then do the global
 // stores (and, fused forward, the leg-piece counting) run — off the MMA's critical path.
@@ -302,7 +324,7 @@ __device__ __forceinline__ void store_rows_staged(const uint32_t (&w)[NW], __nv_
 template <int MODE, int BN, typename Release>
 __device__ __forceinline__ void epilogue_tile(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, bool valid,
                                               __nv_bfloat16* orow, int nb, const amoe_leg& leg, uint32_t stage,
-                                              int lane, uint32_t (&fwd)[2], Release release) {
+                                              int lane, uint32_t (&fwd)[2], PendCount& pend, Release release) {
   constexpr int NW = (MODE == MODE_GATEUP) ? 64 : BN / 2;
   uint32_t w[NW];
   if (MODE == MODE_GATEUP) {
@@ -335,16 +357,11 @@ __device__ __forceinline__ void epilogue_tile(const FfnArgs& args, const DevCtx&
   if (MODE == MODE_GATEUP) {
     store_rows_staged<NW>(w, dst, nb * 128, 128, stage, lane);
   } else {
+    if (args.fuse) flush_count(dc, pend, fwd);      // the previous tile's rows
     store_rows_staged<NW>(w, dst, nb * BN, min(BN, args.out_cols - nb * BN), stage, lane);
     if (args.fuse) {
-      // every lane orders its own stores, then the row's owner lane counts the row's pieces
-      fence_sc(dc.G > 1);
-      __syncwarp();
       const int cols = min(BN, dc.d - nb * BN);
-      if (valid && cols > 0) {
-        leg_pieces_done(dc, leg.home, leg.token_slot, leg.k, (uint32_t)(cols / 128));
-        if (nb == 0) { fwd[0] += 1; fwd[1] += (leg.home != dc.rank); }
-      }
+      if (valid && cols > 0) { pend.leg = leg; pend.pieces = cols / 128; pend.nb = nb; }
     }
   }
 }
@@ -357,9 +374,9 @@ template <int MODE, int BN, typename Release>
 __device__ __forceinline__ void epilogue_unit(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, int split, int ks,
                                               int slot, int rloc, bool valid, __nv_bfloat16* orow, int nb,
                                               const amoe_leg& leg, uint32_t stage, int lane, uint32_t (&fwd)[2],
-                                              Release release) {
+                                              PendCount& pend, Release release) {
   if (split <= 1) {
-    epilogue_tile<MODE, BN>(args, dc, taddr, valid, orow, nb, leg, stage, lane, fwd, release);
+    epilogue_tile<MODE, BN>(args, dc, taddr, valid, orow, nb, leg, stage, lane, fwd, pend, release);
     return;
   }
   constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;      // fp32 columns per partial row
@@ -562,6 +579,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int ew = warp - 4;            // TMEM lane quarter (warp % 4)
     const uint32_t stage = smem_u32(smem + STAGES * STAGE_BYTES + 4096 + ew * 4096);
     uint32_t fwd[2] = {0u, 0u};         // legs forwarded by this thread's rows, of which remote
+    PendCount pend{};
     int acc = 0; uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int t = u / split, ks = u - t * split;
@@ -576,10 +594,11 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const uint32_t taddr = tmem_base + (uint32_t)(acc * 256) + ((uint32_t)(ew * 32) << 16);
       const uint32_t tempty = smem_u32(&bars[2 * STAGES + 2 + acc]);
       epilogue_unit<MODE, BN>(args, dc, taddr, split, ks, t, ew * 32 + lane, valid, orow, nb, leg, stage, lane, fwd,
-                              [&] { epi_release_local(tempty, tid, 128); });
+                              pend, [&] { epi_release_local(tempty, tid, 128); });
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
     if (MODE == MODE_DOWN && args.fuse) {
+      flush_count(dc, pend, fwd);         // the last tile's rows
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         fwd[0] += __shfl_xor_sync(0xffffffffu, fwd[0], o);
@@ -959,6 +978,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     const int ew = warp - 4;
     const uint32_t stage = smem_u32(smem + STAGES2 * STAGE2_BYTES + 4096 + ew * 4096);
     uint32_t fwd[2] = {0u, 0u};
+    PendCount pend{};
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&bars[2 * STAGES2 + 2]), 0);
     for (int it = 0;; ++it) {
@@ -983,7 +1003,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       const uint32_t tempty = tempty_leader0 + (uint32_t)(acc * 8);
       // each CTA's half tile is its own split-K slot: 2 t + crank
       epilogue_unit<MODE, 256>(args, dc, taddr, split, ks, 2 * t + (int)crank, ew * 32 + lane, valid, orow, nb, leg,
-                               stage, lane, fwd, [&] {
+                               stage, lane, fwd, pend, [&] {
                                  __syncwarp();
                                  asm volatile("bar.sync 1, 128;" ::: "memory");
                                  if (tid == 128) mbar_arrive_cluster(tempty);
@@ -991,6 +1011,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
     if (MODE == MODE_DOWN && args.fuse) {
+      flush_count(dc, pend, fwd);         // the last tile's rows
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         fwd[0] += __shfl_xor_sync(0xffffffffu, fwd[0], o);
