@@ -72,7 +72,7 @@ __device__ __forceinline__ void route_select(const float (&v)[kZJ], int E, int K
 // column order, then the xor-tree warp sum). The row stays in registers (<= 16 chunks per lane);
 // lane e % 32 receives z[e] in v[e / 32], the layout route_select expects.
 template <typename T>
-__device__ __forceinline__ void gate_logits(const DevCtx& c, const T* __restrict__ x, const T* __restrict__ wg,
+__device__ __noinline__ void gate_logits(const DevCtx& c, const T* __restrict__ x, const T* __restrict__ wg,
                                             const float* __restrict__ bias, int lane, float (&v)[kZJ]) {
   using V = Vec<T>;
   constexpr int MAXC = 16;
@@ -327,12 +327,58 @@ __global__ void cdrain_kernel(DevCtx c) {
 
 // ---------------------------------------------------------------------------- combine (a8)
 
+// Router gate of a whole chunk on the tensor cores (bf16, every pending token at the same next
+// layer): logits[32][E] = X[32 tokens, d] · Wgᵀ + b with warp-level mma.sync m16n8k16 (bf16 in,
+// fp32 accumulate), fragments loaded straight from the x rows and Wg rows (L2 / L1). Tiles
+// (m16 block, n8 block) go to the warps round-robin; rows of tokens without a gate read row 0.
+__device__ __noinline__ void gate_chunk_mma(const DevCtx& c, const __nv_bfloat16* __restrict__ xbase,
+                                               const int* s_slot, const __nv_bfloat16* __restrict__ wg,
+                                               const float* __restrict__ bias, float* s_z, int zld, int warp,
+                                               int lane) {
+  const int ntiles = 2 * (c.E / 8);
+  const int g = lane >> 2, q = lane & 3;
+  for (int tile = warp; tile < ntiles; tile += kTokWarps) {
+    const int mb = tile & 1, nt = tile >> 1;
+    const int s0 = s_slot[mb * 16 + g], s1 = s_slot[mb * 16 + g + 8];
+    const __nv_bfloat16* x0 = xbase + (uint64_t)(s0 < 0 ? 0 : s0) * c.d + 2 * q;
+    const __nv_bfloat16* x1 = xbase + (uint64_t)(s1 < 0 ? 0 : s1) * c.d + 2 * q;
+    const __nv_bfloat16* wr = wg + (uint64_t)(nt * 8 + g) * c.d + 2 * q;
+    float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll 4
+    for (int k0 = 0; k0 < c.d; k0 += 16) {
+      const uint32_t a0 = *reinterpret_cast<const uint32_t*>(x0 + k0);
+      const uint32_t a1 = *reinterpret_cast<const uint32_t*>(x1 + k0);
+      const uint32_t a2 = *reinterpret_cast<const uint32_t*>(x0 + k0 + 8);
+      const uint32_t a3 = *reinterpret_cast<const uint32_t*>(x1 + k0 + 8);
+      const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wr + k0);
+      const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wr + k0 + 8);
+      asm volatile(
+          "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+          "{%0, %1, %2, %3};"
+          : "+f"(d0), "+f"(d1), "+f"(d2), "+f"(d3)
+          : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    const int col = nt * 8 + 2 * q;
+    const float b0v = bias ? bias[col] : 0.f, b1v = bias ? bias[col + 1] : 0.f;
+    float* z0 = s_z + (mb * 16 + g) * zld;
+    float* z1 = s_z + (mb * 16 + g + 8) * zld;
+    z0[col] = d0 + b0v; z0[col + 1] = d1 + b1v;
+    z1[col] = d2 + b0v; z1[col + 1] = d3 + b1v;
+  }
+}
+
 // KSM: compile-time bound on K+S (2, 4, 8 or 12) sizing the per-chunk leg registers.
 template <typename T, int KSM, bool GATE>
 __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) combine_kernel(DevCtx c, int retire_pass) {
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   __shared__ unsigned long long s_merged, s_retired;
+  // GATE (bf16): tokens whose next layer routes with a gate are routed after the chunk's merges,
+  // their logits computed for the whole chunk at once on the tensor cores
+  constexpr int kZLD = GATE ? AMOE_MAX_E + 1 : 1;
+  __shared__ float s_z[GATE ? kTPC * kZLD : 1];
+  __shared__ int s_gslot[GATE ? kTPC : 1], s_glayer[GATE ? kTPC : 1], s_gpass[GATE ? kTPC : 1];
+  __shared__ int s_guni;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
   const int n = info[0];
@@ -346,12 +392,14 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
   int32_t* tpass = wsp<int32_t>(c, c.rank, c.lay.tok_pass);
   if (threadIdx.x == 0) { s_merged = 0; s_retired = 0; }
   __syncthreads();
+  const bool gate_tc = GATE && c.dtype == AMOE_BF16 && (c.E % 8) == 0;
   for (int chunk = blockIdx.x; chunk * kTPC < n; chunk += gridDim.x) {
     for (int t = 0; t < kTPW; ++t) {
       const int lt = warp * kTPW + t;
       const int i = chunk * kTPC + lt;
       PendingLeg* my = legs + lt * c.KS;
       if (lane < c.KS) my[lane].r = -1;
+      if (GATE && lane == 0) s_gslot[lt] = -1;
       if (i >= n) continue;
       const uint32_t pos = start + (uint32_t)i;
       const amoe_leg e = ring[pos & c.cring_mask];
@@ -415,6 +463,11 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
         }
         continue;
       }
+      if (GATE && gw && gate_tc) {
+        // routed after the chunk's merges (tensor-core gate over the chunk)
+        if (lane == 0) { s_gslot[lt] = slot; s_glayer[lt] = layer; s_gpass[lt] = pass; }
+        continue;
+      }
       if (GATE && gw) {
         // the next layer's gate on the row just normalised (this warp stored x; same lanes)
         gate_logits<T>(c, xbase + (uint64_t)slot * c.d, gw, gb, lane, zv);
@@ -431,6 +484,53 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
       }
       if (lane == 0) wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
       make_legs(c, layer, slot, my_e, my_w, lane, my);
+    }
+    if (gate_tc) {
+      __syncthreads();                    // x rows of the chunk stored, gate list complete
+      if (threadIdx.x == 0) {
+        int u = -2;                       // -2: none pending, -1: mixed layers, else the layer
+        for (int j = 0; j < kTPC; ++j)
+          if (s_gslot[j] >= 0) u = (u == -2 || u == s_glayer[j]) ? s_glayer[j] : -1;
+        s_guni = u;
+      }
+      __syncthreads();
+      const int u = s_guni;
+      if (u >= 0) {
+        const uint64_t* ge = gate_entry(c, u);
+        gate_chunk_mma(c, reinterpret_cast<const __nv_bfloat16*>(xbase), s_gslot,
+                       reinterpret_cast<const __nv_bfloat16*>(ge[0]), reinterpret_cast<const float*>(ge[1]),
+                       s_z, kZLD, warp, lane);
+      }
+      __syncthreads();
+      if (u != -2) {
+        for (int t = 0; t < kTPW; ++t) {
+          const int lt = warp * kTPW + t;
+          const int slot = s_gslot[lt];
+          if (slot < 0) continue;
+          const int layer = s_glayer[lt], pass = s_gpass[lt];
+          float zv[kZJ];
+          if (u >= 0) {
+#pragma unroll
+            for (int j = 0; j < kZJ; ++j) {
+              const int e = lane + kWarp * j;
+              zv[j] = e < c.E ? s_z[lt * kZLD + e] : -INFINITY;
+            }
+          } else {                        // mixed layers in the chunk: per-token gate
+            const uint64_t* ge = gate_entry(c, layer);
+            gate_logits<T>(c, xbase + (uint64_t)slot * c.d, reinterpret_cast<const T*>(ge[0]),
+                           reinterpret_cast<const float*>(ge[1]), lane, zv);
+          }
+          int my_e;
+          float my_w;
+          route_select(zv, c.E, c.K, lane, my_e, my_w);
+          if (lane < c.K) {
+            wsp<int32_t>(c, c.rank, c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = my_e;
+            wsp<float>(c, c.rank, c.lay.tok_w)[(uint64_t)slot * c.K + lane] = my_w;
+          }
+          if (lane == 0) wsp<uint32_t>(c, c.rank, c.lay.legs_done)[slot] = 0;
+          make_legs(c, layer, slot, my_e, my_w, lane, legs + lt * c.KS);
+        }
+      }
     }
     __syncthreads();
     scatter_legs(c, legs, kTPC * c.KS);
