@@ -233,6 +233,46 @@ def test_shared_experts_and_topk6():
     assert floored_err(to_np(ctx.state()["h"]), ref) <= TOL["bf16"]
 
 
+@pytest.mark.parametrize("E,K,S,T,cap", [
+    (1, 1, 0, 300, 0),      # one expert, top-1: the layer is a dense SwiGLU MLP
+    (4, 4, 0, 257, 0),      # K = E: every token visits every expert (ragged T)
+    (8, 1, 0, 130, 0),      # top-1 (no merge barrier beyond one leg)
+    (8, 2, 2, 77, 0),       # shared experts with few tokens
+    (8, 2, 0, 512, 7),      # drain cap: many small executions per queue
+    (16, 3, 1, 33, 0),      # odd K with a shared expert, T just over one warp chunk
+])
+def test_degenerate_configs_match_oracle(E, K, S, T, cap):
+    """Degenerate and ragged routing shapes through the whole native loop, against the oracle's
+    synchronous run (free-running, 2 layers, bf16)."""
+    P = Problem(L=2, E=E, K=K, S=S, d=128, ff=256, T=T, seed=40 + E + K)
+    ctx = P.make_ctx(max_batch=cap)
+    admit(ctx, P)
+    stats = ctx.run(retire_pass=1, policy="mtfs" if cap else "defrag", grouped=not cap)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert stats["token_layers"] == T * 2 and stats["legs"] == T * 2 * (K + S)
+    if cap:
+        assert stats["queues_run"] >= (T * K * 2) // cap
+    W, SH = P.oracle_weights()
+    ref, _ = drivers.sync_run(host_values(P.h0[0], "bf16"), P.logits, W, P.K, n_passes=1, shared=SH)
+    h = to_np(ctx.state()["h"])
+    assert floored_err(h, ref) <= TOL["bf16"]
+    assert row_l2_err(h, ref) <= ROW_L2["bf16"] * 2
+
+
+def test_empty_admission_is_a_noop():
+    """Enqueueing zero tokens and running with nothing admitted returns at once, no launch of the
+    FFN, no fault."""
+    P = Problem(**TINY, seed=41)
+    ctx = P.make_ctx()
+    empty = torch.empty(0, dtype=torch.int32, device="cuda")
+    ctx.enqueue(0, empty, logits=torch.empty(0, P.E, device="cuda"))
+    stats = ctx.run(retire_pass=1)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert stats["token_layers"] == 0 and stats["legs"] == 0 and stats["picks"] == 0
+
+
 # ---------------------------------------------------------------- multi-rank over (loopback) peers
 
 def drive_ranks(ctxs, gbs, P, retire_pass, policy="defrag"):
