@@ -1353,12 +1353,6 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const char* ev = getenv("AMOE_FFN_1CTA");
   const bool force1 = ev ? ev[0] == '1' : kDefault1Cta;
   const bool pair = !force1 && c.d % 256 == 0 && num_sms >= 2;
-  // raster group: rows of a queue sharing a weight slab through L2. 4096 rows: the lowest DRAM
-  // traffic measured (gate/up 11.5 GB vs 15.5 GB at 2048 on a Mixtral layer), which under the
-  // power cap buys SM clock (+4.5% FFN throughput; profiles/r01_group_m_sweep.md)
-  const char* eg = getenv(part == 2 && getenv("AMOE_GROUP_M_DOWN") ? "AMOE_GROUP_M_DOWN" : "AMOE_GROUP_M");
-  const int gm_rows = eg ? atoi(eg) : 4096;
-  a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
     a.n_tiles = c.ff / 128;
@@ -1389,6 +1383,13 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const int smode = !ed || !strcmp(ed, "auto") ? (a.k_blocks >= 64 ? 3 : 0)
                     : !strcmp(ed, "dynamic") ? 3 : !strcmp(ed, "die") ? (c.die_cnt[1] > 0 ? 1 : 3) : 0;
   a.die_sched = smode;
+  // raster group: rows of a queue sharing a weight slab through L2. 4096 rows: the lowest DRAM
+  // traffic measured for the static raster (gate/up 11.5 GB vs 15.5 GB at 2048 on a Mixtral layer,
+  // profiles/r01_group_m_sweep.md); under the dynamic schedule the down GEMM (7 MB token slabs)
+  // reads least with 2048-row groups (5.8-6.1 vs 8.3-8.5 GB, bench +0.8 %)
+  const char* eg = getenv(part == 2 && getenv("AMOE_GROUP_M_DOWN") ? "AMOE_GROUP_M_DOWN" : "AMOE_GROUP_M");
+  const int gm_rows = eg ? atoi(eg) : (part == 2 && pair && smode ? 2048 : 4096);
+  a.group_m = std::max(1, gm_rows / (pair ? 256 : 128));
   if (pair) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(num_sms & ~1));
