@@ -27,8 +27,8 @@ def _run_layer(P, ctx):
     slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
     ctx.token_init(slots, dev_tensor(P.h0[0], P.dtype), 0)
     ctx.enqueue(0, slots, logits=torch.from_numpy(np.ascontiguousarray(P.tables[0][0, 0])).cuda())
-    gb = amoe.GroupBuffers(ctx, P.T * P.K + 128 * P.E)
-    gb.set_queues([(0, e) for e in range(P.E)])
+    gb = amoe.GroupBuffers(ctx, P.T * (P.K + P.S) + 128 * (P.E + P.S))
+    gb.set_queues([(0, e) for e in range(P.E + P.S)])
     ctx.rebatch(gb)
     ctx.expert_ffn(gb)
     torch.cuda.synchronize()
@@ -207,18 +207,25 @@ def test_split_k_cold_expert(pair, d, ff, T):
 
 
 @pytest.mark.slow
-def test_mixtral_layer_fullsize_sampled():
-    P = Problem(L=1, E=8, K=2, S=0, d=4096, ff=14336, T=16384, seed=12, n_tab=1)
+@pytest.mark.parametrize("shape", ["mixtral", "deepseek"])
+def test_layer_fullsize_sampled(shape):
+    """One full-size layer in the bench's launch configuration (grouped pick, CTA-pair kernels,
+    the schedule `auto` picks for the shape): counts = router histogram, sampled rows of every
+    queue against the oracle, and the merge of every token bit-exact."""
+    if shape == "mixtral":
+        P = Problem(L=1, E=8, K=2, S=0, d=4096, ff=14336, T=16384, seed=12, n_tab=1)
+    else:
+        P = Problem(L=1, E=64, K=6, S=2, d=2048, ff=1408, T=16384, seed=13, n_tab=1)
     ctx = P.make_ctx()
     gb = _run_layer(P, ctx)
     n, off, _ = gb.info()
     idx, w = nx.route_topk(P.logits(0, 0), P.K)
-    hist = np.bincount(idx.ravel(), minlength=P.E)
+    hist = np.concatenate([np.bincount(idx.ravel(), minlength=P.E), np.full(P.S, P.T)])
     assert np.array_equal(n, hist)                              # counts = router histogram
     meta = gb.meta.cpu().numpy()
     x = ctx.state()["x"]
     g = np.random.default_rng(0)
-    for i in range(P.E):
+    for i in range(P.E + P.S):
         # sampled rows: first, last and two random rows of every expert's segment
         picks = sorted({0, n[i] - 1, *g.integers(0, n[i], 2).tolist()})
         rows = off[i] + np.array(picks)
@@ -238,7 +245,8 @@ def test_mixtral_layer_fullsize_sampled():
     torch.cuda.synchronize()
     ctx.check()
     st = ctx.state()
-    ref_h = nx.combine(h_before, w_gpu, to_np(st["pool"]), None, "bf16")
+    pool = to_np(st["pool"])
+    ref_h = nx.combine(h_before, w_gpu, pool[:, :P.K], pool[:, P.K:] if P.S else None, "bf16")
     assert np.array_equal(to_np(st["h"]), ref_h)
     assert int(st["stats"][1]) == P.T                          # L = 1: every token retired
 
