@@ -853,9 +853,13 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   auto publish = [&](int it, int4 rec) {
     const int slot = it % RING;
     mbar_wait_cluster(smem_u32(&ring_empty[slot]), ((it / RING) & 1) ^ 1u);
-    const uint32_t a_loc = smem_u32(&ring[slot]);
-    st_cluster_v4(mapa(a_loc, 1), rec);                           // the peer's copy: cluster scope
-    mbar_arrive_cluster(mapa(smem_u32(&ring_full[slot]), 1));
+    // the peer's copy: an asynchronous remote store that completes the peer's barrier phase
+    // itself (st.async + expect_tx): no cluster-scope release fence on the producer's path
+    const uint32_t pf = mapa(smem_u32(&ring_full[slot]), 1);
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], 16;" :: "r"(pf) : "memory");
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.s32 [%0], {%1, %2, %3, %4}, [%5];"
+                 :: "r"(mapa(smem_u32(&ring[slot]), 1)), "r"(rec.x), "r"(rec.y), "r"(rec.z), "r"(rec.w), "r"(pf)
+                 : "memory");
     ring[slot] = rec;                                              // the leader's copy: CTA scope
     mbar_arrive(smem_u32(&ring_full[slot]));
   };
@@ -882,10 +886,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   // rows), stalling the epilogue for microseconds per unit.
   auto ring_get = [&](int it) -> int4 {
     const int slot = it % RING;
-    // the leader's consumers synchronise with a same-CTA producer (CTA-scope acquire: no L1
-    // invalidation); the peer's with a remote one (cluster scope)
-    if (leader) mbar_wait(smem_u32(&ring_full[slot]), (it / RING) & 1);
-    else mbar_wait_cluster(smem_u32(&ring_full[slot]), (it / RING) & 1);
+    // CTA-scope waits: the leader's copy comes from a same-CTA producer, the peer's through the
+    // barrier's own transaction count (st.async), as TMA data does
+    mbar_wait(smem_u32(&ring_full[slot]), (it / RING) & 1);
     const int4 rec = lds_v4(smem_u32(&ring[slot]));
     // (rec.x is a queue index or -1, never INT_MIN: the select is 0, but the address depends on
     // the loaded value, so the arrive cannot be performed before the load)
