@@ -1374,16 +1374,16 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     a.fuse = fuse;
   }
   // Tile schedule of the CTA-pair kernels (AMOE_FFN_SCHED, read per launch):
-  //   auto (default): dynamic where weight slabs are long (K >= 4096, Mixtral-shaped GEMMs),
-  //                   static raster otherwise (short units made the claim cost visible)
+  //   auto / dynamic (default): clusters claim the next raster unit from one atomic counter and
+  //             hand it to the pair's roles through the shared-memory unit ring — the
+  //             concurrently running units stay adjacent, so weight and token slabs are shared
+  //             in L2 while hot (Mixtral gate/up DRAM reads 6.5-13 -> 3.1 GB per layer, tensor
+  //             pipe 96.7 -> 98.4 % busy; DeepSeek down 78 -> 85 %)
   //   static  : cluster c takes units c, c + #clusters, ... of the raster
-  //   dynamic : clusters claim the next raster unit from one atomic counter — the concurrently
-  //             running units stay adjacent, so weight and token slabs are shared in L2 while
-  //             hot (Mixtral: gate/up DRAM reads 6.5-10.9 -> 3.1 GB per layer; bench +6.5 %)
   //   die     : as dynamic, with each die owning its share of every queue's N tiles (needs a
   //             measured die split; otherwise dynamic)
   const char* ed = getenv("AMOE_FFN_SCHED");
-  const int smode = !ed || !strcmp(ed, "auto") ? (a.k_blocks >= 64 ? 3 : 0)
+  const int smode = !ed || !strcmp(ed, "auto") ? 3
                     : !strcmp(ed, "dynamic") ? 3 : !strcmp(ed, "die") ? (c.die_cnt[1] > 0 ? 1 : 3) : 0;
   a.die_sched = smode;
   // raster group: rows of a queue sharing a weight slab through L2. 4096 rows: the lowest DRAM
