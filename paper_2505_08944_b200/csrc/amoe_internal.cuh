@@ -248,6 +248,35 @@ template <> struct Vec<float> {
   }
 };
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every libamoe kernel is launched with programmatic stream serialisation (launch_pdl): it may be
+// scheduled while the previous kernel of the stream drains, runs AMOE_PDL_ENTRY first — wait
+// until that kernel completed and its memory is visible, then let the next kernel be scheduled —
+// so a kernel boundary costs no launch latency. (griddepcontrol.* are no-ops for normal launches.)
+#define AMOE_PDL_ENTRY()                                                      \
+  do {                                                                         \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                         \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");            \
+  } while (0)
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -24,6 +24,7 @@ struct SimtArgs {
 };
 
 __global__ void __launch_bounds__(THREADS) ffn_simt_kernel(SimtArgs a) {
+  AMOE_PDL_ENTRY();
   __shared__ float As[TK][TM + 1];
   __shared__ float Bs[TK][TN + 1];
   __shared__ float Cs[TK][TN + 1];
@@ -110,10 +111,10 @@ int launch_ffn_simt(const DevCtx& c, int nq, const int32_t* qinfo, const int* ws
   for (int q = 0; q < nq; ++q) a.wslot[q] = wslot[q];
   a.mode = 0; a.N = c.ff; a.Kd = c.d;
   a.in = (const float*)tile; a.out = (float*)act;
-  simt::ffn_simt_kernel<<<num_sms * 4, simt::THREADS, 0, s>>>(a);
+  launch_pdl(simt::ffn_simt_kernel, dim3(num_sms * 4), dim3(simt::THREADS), 0, s, a);
   a.mode = 1; a.N = c.d; a.Kd = c.ff;
   a.in = (const float*)act; a.out = (float*)out;
-  simt::ffn_simt_kernel<<<num_sms * 4, simt::THREADS, 0, s>>>(a);
+  launch_pdl(simt::ffn_simt_kernel, dim3(num_sms * 4), dim3(simt::THREADS), 0, s, a);
   return 2;
 }
 

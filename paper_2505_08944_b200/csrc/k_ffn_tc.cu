@@ -430,6 +430,7 @@ template <int MODE, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmA32, const FfnArgs args,
               const __grid_constant__ DevCtx dc) {
+  AMOE_PDL_ENTRY();
   __shared__ unsigned long long s_fwd[2];     // legs forwarded, of which remote
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -726,6 +727,7 @@ struct Sched2 {
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
+  AMOE_PDL_ENTRY();
   __shared__ unsigned long long s_fwd[2];
   __shared__ int4 s_epi_rec[1];            // die schedule: the epilogue's current unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1054,6 +1056,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
 template <int MODE, int BN, bool PAIR>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const FfnArgs args, const __grid_constant__ DevCtx dc,
                                                             int slots) {
+  AMOE_PDL_ENTRY();
   constexpr int BMx = PAIR ? 256 : 128;
   constexpr int HALVES = PAIR ? 2 : 1;
   constexpr int W = (MODE == MODE_GATEUP) ? 256 : BN;        // partial row width (fp32)
@@ -1399,30 +1402,32 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = tc2::SMEM2_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     const int slots = (num_sms & ~1) / 2;
     if (part == 1) {
       cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
-      if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
+      if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_GATEUP, 256, true>, dim3(num_sms * 2), dim3(256), 0, s, a, c, slots);
     } else {
       cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
-      if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, true><<<num_sms * 2, 256, 0, s>>>(a, c, slots);
+      if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 256, true>, dim3(num_sms * 2), dim3(256), 0, s, a, c, slots);
     }
     return a.allow_split ? 2 : 1;
   }
   if (part == 1) {
-    ffn_tc_kernel<MODE_GATEUP, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_tile, tm_tile32, a, c);
-    if (a.allow_split) splitk_reduce_kernel<MODE_GATEUP, 256, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
+    launch_pdl(ffn_tc_kernel<MODE_GATEUP, 256>, dim3(num_sms), dim3(THREADS), SMEM_BYTES, s, tm_tile, tm_tile32, a, c);
+    if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_GATEUP, 256, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
   } else if (bn == 256) {
-    ffn_tc_kernel<MODE_DOWN, 256><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, tm_act32, a, c);
-    if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 256, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
+    launch_pdl(ffn_tc_kernel<MODE_DOWN, 256>, dim3(num_sms), dim3(THREADS), SMEM_BYTES, s, tm_act, tm_act32, a, c);
+    if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 256, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
   } else {
-    ffn_tc_kernel<MODE_DOWN, 128><<<num_sms, THREADS, SMEM_BYTES, s>>>(tm_act, tm_act32, a, c);
-    if (a.allow_split) splitk_reduce_kernel<MODE_DOWN, 128, false><<<num_sms * 2, 256, 0, s>>>(a, c, num_sms);
+    launch_pdl(ffn_tc_kernel<MODE_DOWN, 128>, dim3(num_sms), dim3(THREADS), SMEM_BYTES, s, tm_act, tm_act32, a, c);
+    if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 128, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
   }
   return a.allow_split ? 2 : 1;
 }

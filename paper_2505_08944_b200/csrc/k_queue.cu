@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // k_queue.cu — expert-side µ-queue kernels (owner rank):
 //   drain   : a4 step 1 — take the published FIFO prefix of each selected µ-queue (PAPER.md
 //             L222 "executor drains the selected queue"), allot 128-aligned rows per queue
@@ -11,10 +12,21 @@
 
 namespace amoe {
 
+// AMOE_PDL=0 launches every kernel without programmatic dependent launch (A/B)
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("AMOE_PDL");
+    on = e ? (e[0] != '0') : 1;
+  }
+  return on != 0;
+}
+
 
 constexpr int kDrainThreads = 128;
 
 __global__ void __launch_bounds__(kDrainThreads) drain_kernel(DevCtx c, GroupDev g) {
+  AMOE_PDL_ENTRY();
   __shared__ uint32_t avail[AMOE_MAX_GROUP], head[AMOE_MAX_GROUP], rv[AMOE_MAX_GROUP];
   __shared__ int slow[AMOE_MAX_GROUP];
   __shared__ int nslow;
@@ -89,6 +101,7 @@ __device__ __forceinline__ int find_queue(const int* pre, int nq, int r) {
 constexpr int kRowThreads = 256;
 
 __global__ void __launch_bounds__(kRowThreads) gather_kernel(DevCtx c, GroupDev g) {
+  AMOE_PDL_ENTRY();
   __shared__ int pre[AMOE_MAX_GROUP + 1];
   __shared__ int n_s[AMOE_MAX_GROUP], off_s[AMOE_MAX_GROUP], start_s[AMOE_MAX_GROUP];
   if (threadIdx.x == 0) {
@@ -123,6 +136,7 @@ __global__ void __launch_bounds__(kRowThreads) gather_kernel(DevCtx c, GroupDev 
 }
 
 __global__ void __launch_bounds__(kRowThreads) forward_kernel(DevCtx c, GroupDev g) {
+  AMOE_PDL_ENTRY();
   __shared__ int pre[AMOE_MAX_GROUP + 1];
   __shared__ int off_s[AMOE_MAX_GROUP];
   __shared__ unsigned long long s_legs, s_remote;
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(kRowThreads) forward_kernel(DevCtx c, GroupDev
 }
 
 int launch_drain(const DevCtx& c, const GroupDev& g, cudaStream_t s) {
-  drain_kernel<<<1, kDrainThreads, 0, s>>>(c, g);
+  launch_pdl(drain_kernel, dim3(1), dim3(kDrainThreads), 0, s, c, g);
   return 1;
 }
 
@@ -177,12 +191,12 @@ static int row_grid(const DevCtx& c, int num_sms) {
 }
 
 int launch_gather(const DevCtx& c, const GroupDev& g, int num_sms, cudaStream_t s) {
-  gather_kernel<<<row_grid(c, num_sms), kRowThreads, 0, s>>>(c, g);
+  launch_pdl(gather_kernel, dim3(row_grid(c, num_sms)), dim3(kRowThreads), 0, s, c, g);
   return 1;
 }
 
 int launch_forward(const DevCtx& c, const GroupDev& g, int num_sms, cudaStream_t s) {
-  forward_kernel<<<row_grid(c, num_sms), kRowThreads, 0, s>>>(c, g);
+  launch_pdl(forward_kernel, dim3(row_grid(c, num_sms)), dim3(kRowThreads), 0, s, c, g);
   return 1;
 }
 

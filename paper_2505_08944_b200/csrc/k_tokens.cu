@@ -205,6 +205,7 @@ __device__ __forceinline__ void rmsnorm_row(const DevCtx& c, const T* h, T* x, f
 template <typename T>
 __global__ void __launch_bounds__(kTokThreads) token_init_kernel(DevCtx c, const int32_t* __restrict__ slots,
                                                                  int n, const T* __restrict__ h0, int pass) {
+  AMOE_PDL_ENTRY();
   using V = Vec<T>;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(kTokThreads) enqueue_kernel(DevCtx c, int laye
                                                               int n, const float* __restrict__ logits,
                                                               const int32_t* __restrict__ tidx,
                                                               const float* __restrict__ tw) {
+  AMOE_PDL_ENTRY();
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int chunk = blockIdx.x; chunk * kTPC < n; chunk += gridDim.x) {
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(kTokThreads) enqueue_kernel(DevCtx c, int laye
 // writes (release/acquire), and when commit != reserve (a producer mid-flight on a peer) the
 // published prefix is found by scanning the per-entry seq flags.
 __global__ void cdrain_kernel(DevCtx c) {
+  AMOE_PDL_ENTRY();
   uint32_t* ctr = wsp<uint32_t>(c, c.rank, c.lay.cctr);
   amoe_leg* ring = wsp<amoe_leg>(c, c.rank, c.lay.cring);
   int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
@@ -370,6 +373,7 @@ __device__ __noinline__ void gate_chunk_mma(const DevCtx& c, const __nv_bfloat16
 // KSM: compile-time bound on K+S (2, 4, 8 or 12) sizing the per-chunk leg registers.
 template <typename T, int KSM, bool GATE>
 __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) combine_kernel(DevCtx c, int retire_pass) {
+  AMOE_PDL_ENTRY();
   using V = Vec<T>;
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   __shared__ unsigned long long s_merged, s_retired;
@@ -547,6 +551,7 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
 // AMOE_SYNC layer-barrier sequence). Release: the stores of this rank's earlier kernels are
 // visible to a peer that observes the flag.
 __global__ void announce_kernel(DevCtx c, uint32_t value, int base) {
+  AMOE_PDL_ENTRY();
   const int r = threadIdx.x;
   if (r < c.G) st_release(wsp<uint32_t>(c, r, c.lay.done) + base + c.rank, value, r != c.rank);
 }
@@ -557,9 +562,9 @@ int launch_token_init(const DevCtx& c, const int32_t* slots, int n, const void* 
   const int grid = (n + kTokWarps - 1) / kTokWarps < 1184 ? (n + kTokWarps - 1) / kTokWarps : 1184;
   if (n <= 0) return 0;
   if (c.dtype == AMOE_BF16)
-    token_init_kernel<__nv_bfloat16><<<grid, kTokThreads, 0, s>>>(c, slots, n, (const __nv_bfloat16*)h0, pass);
+    launch_pdl(token_init_kernel<__nv_bfloat16>, dim3(grid), dim3(kTokThreads), 0, s, c, slots, n, (const __nv_bfloat16*)h0, pass);
   else
-    token_init_kernel<float><<<grid, kTokThreads, 0, s>>>(c, slots, n, (const float*)h0, pass);
+    launch_pdl(token_init_kernel<float>, dim3(grid), dim3(kTokThreads), 0, s, c, slots, n, (const float*)h0, pass);
   return 1;
 }
 
@@ -568,7 +573,7 @@ int launch_enqueue(const DevCtx& c, int layer, const int32_t* slots, int n, cons
   if (n <= 0) return 0;
   int grid = (n + kTPC - 1) / kTPC;
   if (grid > 1184) grid = 1184;
-  enqueue_kernel<<<grid, kTokThreads, 0, s>>>(c, layer, slots, n, logits, tidx, tw);
+  launch_pdl(enqueue_kernel, dim3(grid), dim3(kTokThreads), 0, s, c, layer, slots, n, logits, tidx, tw);
   return 1;
 }
 
@@ -586,7 +591,7 @@ static void launch_combine_t(const DevCtx& c, int retire_pass, cudaStream_t s) {
   }
   int grid = (c.T + kTPC - 1) / kTPC;
   if (grid > sms * occ) grid = sms * occ;
-  combine_kernel<T, KSM, GATE><<<grid, kTokThreads, 0, s>>>(c, retire_pass);
+  launch_pdl(combine_kernel<T, KSM, GATE>, dim3(grid), dim3(kTokThreads), 0, s, c, retire_pass);
 }
 
 template <typename T, bool GATE>
@@ -599,7 +604,7 @@ static void launch_combine_g(const DevCtx& c, int retire_pass, cudaStream_t s) {
 }
 
 int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
-  cdrain_kernel<<<1, 32, 0, s>>>(c);
+  launch_pdl(cdrain_kernel, dim3(1), dim3(32), 0, s, c);
   if (c.dtype == AMOE_BF16) {
     if (c.gate_on) launch_combine_g<__nv_bfloat16, true>(c, retire_pass, s);
     else launch_combine_g<__nv_bfloat16, false>(c, retire_pass, s);
@@ -611,7 +616,7 @@ int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
 }
 
 int launch_announce(const DevCtx& c, uint32_t value, int base, cudaStream_t s) {
-  announce_kernel<<<1, 32, 0, s>>>(c, value, base);
+  launch_pdl(announce_kernel, dim3(1), dim3(32), 0, s, c, value, base);
   return 1;
 }
 
