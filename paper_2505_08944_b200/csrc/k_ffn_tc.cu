@@ -839,15 +839,21 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   // leader producer: claims are issued one unit ahead (the atomic's latency overlaps the
   // current unit's loads) and resolved — own die first, then the other die's list — into the
   // unit published to both CTAs' rings one unit ahead of its loads
-  const int my_die = (int)((dc.die_mask[smid_u32() >> 6] >> (smid_u32() & 63)) & 1ull);
+  // single list (die_sched == 3): every cluster's first unit is its own index (no claim), the
+  // counter hands out units ncl, ncl + 1, ... — a cluster that pre-claims its second unit at
+  // the start can then never take a first unit from another (with fewer units than 2 x clusters
+  // the claim-ahead alone left half the clusters idle and doubled the kernel time)
+  const bool single = args.die_sched == 3;
+  const int my_die = single ? 0 : (int)((dc.die_mask[smid_u32() >> 6] >> (smid_u32() & 63)) & 1ull);
+  const uint32_t claim_base = single ? (uint32_t)ncl : 0u;
   int claim_d = my_die;
   uint32_t claim_u = 0;
-  auto issue_claim = [&]() { claim_u = atomicAdd(args.sched + claim_d, 1u); };
+  auto issue_claim = [&]() { claim_u = atomicAdd(args.sched + claim_d, 1u) + (claim_d == 0 ? claim_base : 0u); };
   auto resolve_claim = [&]() -> int4 {
     for (;;) {
       const int ud = die_units(claim_d);
       if (claim_u < (uint32_t)ud) return die_unit(claim_d, (int)claim_u);
-      if (claim_d != my_die) return make_int4(-1, 0, 0, 0);     // both lists exhausted
+      if (single || claim_d != my_die) return make_int4(-1, 0, 0, 0);   // no list left
       claim_d = 1 - my_die;                                     // steal
       issue_claim();
     }
@@ -868,10 +874,17 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   int4 next_unit = make_int4(-1, 0, 0, 0);
   auto claim_publish = [&](int it) -> int4 {
     if (it == 0) {                         // unit 0 now; the claim for unit 1 in flight
-      issue_claim();
+      if (single) {
+        claim_u = (uint32_t)cl;
+      } else {
+        issue_claim();
+      }
       next_unit = resolve_claim();
       publish(0, next_unit);
-      if (next_unit.x >= 0) issue_claim();
+      if (next_unit.x >= 0) {
+        if (single && units <= ncl) claim_u = ~0u;   // one round: no second unit to claim
+        else issue_claim();
+      }
     }
     return next_unit;                      // published one unit ago
   };
@@ -882,6 +895,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     publish(it + 1, next_unit);
     if (next_unit.x >= 0) issue_claim();
   };
+  // (claim_u = ~0u resolves to the end record without an atomic)
   // every other role (one thread): take unit `it` from this CTA's ring, free the slot. The free
   // is a relaxed arrive ordered after the record load by a dependency on its value: a release
   // arrive would first drain this thread's outstanding global stores (the epilogue's output
