@@ -300,9 +300,9 @@ amoe_status amoe_scratch_group(amoe_ctx_t ctx, amoe_group* grp);
 int64_t amoe_launch_count(amoe_ctx_t ctx);
 
 /* SMs per die of the current device as measured by the library's L2-latency probe (run once per
- * device at the first amoe_create): counts[1] == 0 means no die split was detected and the
- * CTA-pair FFN kernels use the static schedule; otherwise each die's CTA pairs claim units of
- * their own share of the weight slabs. AMOE_DIE_SCHED=0 disables the probe. */
+ * device at the first amoe_create): counts[1] == 0 means no die split was detected. The split
+ * is used by the optional die-aware FFN schedule (AMOE_FFN_SCHED=die); the
+ * default dynamic schedule does not need it. AMOE_DIE_PROBE=0 skips the probe. */
 amoe_status amoe_die_info(int32_t counts[2]);
 
 /* Synchronise the context's last stream and report a latched device fault (AMOE_EDEVICE). */

@@ -1262,7 +1262,7 @@ int die_map(uint64_t mask[4], int counts[2]) {
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     c_cnt[0] = nsm;
-    const char* env = getenv("AMOE_DIE_SCHED");
+    const char* env = getenv("AMOE_DIE_PROBE");
     uint32_t *buf = nullptr, *lat = nullptr;
     int* sms = nullptr;
     bool ok = (!env || env[0] != '0') && nsm <= 256 &&
