@@ -130,3 +130,79 @@ def test_async_every_leg_drained_once():
     _, box, _ = drivers.async_run(h0, logits, W, K=2, G=2, T=4, n_passes=2, seed=2, max_cap=2)
     drained = [(g.token, g.layer, g.pass_idx, g.k) for (_, _, _, legs) in box.trace_drain for g in legs]
     assert len(drained) == len(set(drained)) == 8 * 3 * 2 * 2
+
+
+def _every_schedule(h0, logits, W, K, L, cap_choices):
+    """Depth-first over every execution order of the µ-queue model on one GPU: at each step any
+    nonempty (layer, expert) queue may be drained, with any cap in cap_choices (0 = drain all);
+    a token merges as soon as its K legs are home (merge timing cannot change a per-token
+    result). Yields the final h of every complete schedule."""
+    E = len(W[0])
+    N = h0.shape[0]
+
+    def admit(st, toks, l):
+        toks = np.array(sorted(toks))
+        st["x"][toks] = nx.rmsnorm(st["h"][toks])
+        idx, w = nx.route_topk(logits(0, l)[toks], K)
+        st["w"][toks] = w
+        for i, t in enumerate(toks):
+            for k in range(K):
+                st["q"][(l, int(idx[i, k]))].append((int(t), k))
+
+    st0 = {"h": np.asarray(h0, np.float32).copy(), "x": np.zeros_like(h0, dtype=np.float32),
+           "w": np.zeros((N, K), np.float32), "layer": [0] * N, "pool": {},
+           "q": {(l, e): [] for l in range(L) for e in range(E)}, "left": N}
+    admit(st0, range(N), 0)
+
+    def step(st):
+        if st["left"] == 0:
+            yield st["h"]
+            return
+        for (l, e), q in sorted(st["q"].items()):
+            if not q:
+                continue
+            for cap in cap_choices:
+                if cap and cap >= len(q):
+                    continue                        # the same as draining all
+                n = len(q) if cap == 0 else cap
+                s2 = {"h": st["h"].copy(), "x": st["x"], "w": st["w"].copy(), "layer": list(st["layer"]),
+                      "pool": {t: dict(v) for t, v in st["pool"].items()},
+                      "q": {kk: list(v) for kk, v in st["q"].items()}, "left": st["left"]}
+                s2["x"] = st["x"].copy()
+                legs = s2["q"][(l, e)][:n]
+                s2["q"][(l, e)] = s2["q"][(l, e)][n:]
+                toks = np.array([t for t, _ in legs])
+                out = nx.expert_ffn(s2["x"][toks], *W[l][e])
+                done = []
+                for (t, k), row in zip(legs, out):
+                    s2["pool"].setdefault(t, {})[k] = row
+                    if len(s2["pool"][t]) == K:
+                        done.append(t)
+                nxt = []
+                for t in done:
+                    lg = s2["pool"].pop(t)
+                    s2["h"][t] = nx.combine(s2["h"][t:t + 1], s2["w"][t:t + 1],
+                                            np.stack([lg[k] for k in range(K)])[None])[0]
+                    s2["layer"][t] += 1
+                    if s2["layer"][t] == L:
+                        s2["left"] -= 1
+                    else:
+                        nxt.append(t)
+                for lyr in sorted({s2["layer"][t] for t in nxt}):
+                    admit(s2, [t for t in nxt if s2["layer"][t] == lyr], lyr)
+                yield from step(s2)
+
+    yield from step(st0)
+
+
+@pytest.mark.parametrize("T,E,caps,expect", [(3, 3, (0,), 12), (4, 4, (0,), 380), (3, 2, (0, 1), 38780)])
+def test_async_equals_sync_over_every_schedule(T, E, caps, expect):
+    """Brute force (SURVEY.md §8(c) pins): every drain order (and, in the second case, every
+    drain cap) of a tiny 2-layer top-2 problem gives the synchronous result bit for bit."""
+    h0, logits, W, _ = _tiny_problem(100 + T * E, N=T, E=E)
+    ref, _ = drivers.sync_run(h0, logits, W, K=2, n_passes=1)
+    n = 0
+    for h in _every_schedule(h0, logits, W, K=2, L=2, cap_choices=caps):
+        assert np.array_equal(h, ref)
+        n += 1
+    assert n == expect, n          # schedules enumerated for this seeded routing
