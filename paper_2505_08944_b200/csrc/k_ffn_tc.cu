@@ -790,6 +790,11 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&tmA);
   }
+  // this CTA's weight tensor maps of every queue (a grouped launch may hold 66 of them): fetched
+  // now instead of on each queue's first TMA load
+  if (warp == 3)
+    for (int q = lane; q < nq; q += kWarp)
+      tma_prefetch(args.wmaps + args.wslot[q] + args.w_which + (MODE == MODE_GATEUP ? (int)crank : 0));
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
                  :: "r"(smem_u32(tmem_holder)), "r"(TMEM_COLS) : "memory");
