@@ -42,3 +42,14 @@ def test_exponential_skew_variant():
     perm = wl.layer_perm(0, 0, 0, 8)
     # argmax of log p + Gumbel is a draw from p: the top-1 share of each expert matches p
     assert np.abs(top1[perm] - p).max() < 0.015
+
+
+def test_hottest_expert_share_matches_survey():
+    """Zipf s = 1.2 routing (Gumbel-top-k): the hottest expert's share of all legs is ≈ 0.3524
+    for E = 8, K = 2 and ≈ 0.1516 for E = 64, K = 6 (SURVEY.md §8(c) pins, Monte Carlo there);
+    20000 tokens give a standard error below 0.003."""
+    for E, K, share in [(8, 2, 0.3524), (64, 6, 0.1516)]:
+        z = wl.router_logits(0, 1, 20000, E)[0]
+        idx = np.argsort(-z, axis=1, kind="stable")[:, :K]
+        got = np.bincount(idx.ravel(), minlength=E).max() / idx.size
+        assert abs(got - share) < 0.006, (E, K, got)
