@@ -117,6 +117,10 @@ typedef struct amoe_group {
   int32_t* qinfo;                    /* device [3 * AMOE_MAX_GROUP]: n[q], row_off[q], start[q] */
   void* act;                         /* device [rows_cap, ff]: SwiGLU activations */
   void* out;                         /* device [rows_cap, d]: expert outputs */
+  int32_t max_rows_hint;             /* largest queue length expected (0 = unknown), a
+                                        performance hint: <= 128 selects the 1-CTA (M = 128)
+                                        FFN kernels, which stream cold-expert weights faster;
+                                        any n remains correct */
 } amoe_group;
 
 typedef struct amoe_run_params {

@@ -41,7 +41,7 @@ class Leg(C.Structure):
 class Group(C.Structure):
     _fields_ = [("nq", C.c_int32), ("layer", C.c_int32 * MAX_GROUP), ("expert", C.c_int32 * MAX_GROUP),
                 ("rows_cap", C.c_int32), ("tile", C.c_void_p), ("meta", C.c_void_p), ("qinfo", C.c_void_p),
-                ("act", C.c_void_p), ("out", C.c_void_p)]
+                ("act", C.c_void_p), ("out", C.c_void_p), ("max_rows_hint", C.c_int32)]
 
 
 class RunParams(C.Structure):
@@ -190,7 +190,8 @@ class GroupBuffers:
         self.g.tile, self.g.meta, self.g.qinfo = self.tile.data_ptr(), self.meta.data_ptr(), self.qinfo.data_ptr()
         self.g.act, self.g.out = self.act.data_ptr(), self.out.data_ptr()
 
-    def set_queues(self, pairs):
+    def set_queues(self, pairs, max_rows_hint=0):
+        self.g.max_rows_hint = max_rows_hint
         self.g.nq = len(pairs)
         for i, (l, e) in enumerate(pairs):
             self.g.layer[i], self.g.expert[i] = l, e

@@ -96,6 +96,7 @@ struct FfnLaunch {
   const int32_t* qinfo;
   const CUtensorMap* wmaps;      // device [L*H][3]
   int wslot[AMOE_MAX_GROUP];     // (l*H + lq) * 3
+  int rows_hint;                 // amoe_group::max_rows_hint
 };
 
 template <typename T>

@@ -510,6 +510,7 @@ static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaSt
     f.qinfo = g->qinfo;
     f.wmaps = reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps);
     for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
+    f.rows_hint = gathered ? 0 : g->max_rows_hint;
     {
       StageTimer tm(c, ST_GATEUP, s);
       c->launches += launch_ffn_tc(c->dc, f, mt, ma, mt32, ma32, g->act, g->out, g->meta, 0, gathered, c->num_sms, s, 1);
@@ -780,6 +781,13 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
           for (int e = 0; e < c->cfg.E; ++e)
             if (c->dc.owner[e] == c->cfg.rank && c->dc.lq[e] == q) g.expert[0] = e;
         g.nq = 1;
+      }
+      // performance hint for the FFN kernel choice: the largest published queue at this pick
+      // (a drain takes at least that many; single-rank waves take exactly that many)
+      g.max_rows_hint = 0;
+      for (int j = 0; j < g.nq; ++j) {
+        const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
+        g.max_rows_hint = std::max<int32_t>(g.max_rows_hint, (int32_t)Q[(size_t)g.layer[j] * H + lq]);
       }
       const int64_t l0 = c->launches;
       if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;

@@ -1377,7 +1377,12 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   // CTA-pair kernels need d % 256 == 0 and an even grid; AMOE_FFN_1CTA=1 forces 1-CTA, =0 pairs
   const char* ev = getenv("AMOE_FFN_1CTA");
   const bool force1 = ev ? ev[0] == '1' : kDefault1Cta;
-  const bool pair = !force1 && c.d % 256 == 0 && num_sms >= 2;
+  // cold launches (every queue <= 128 rows, by the caller's hint) run the 1-CTA kernels: their
+  // 4 stages hold 128 KB of weights in flight per SM (the pair's 6 stages hold 96 KB next to the
+  // token rows), and grouped cold experts stream at 0.82-0.93 of the HBM roofline instead of
+  // 0.70-0.77 (profiles/r01_rebatch_sweep.md)
+  const bool cold = f.rows_hint > 0 && f.rows_hint <= 128 && !gathered;
+  const bool pair = !force1 && !cold && c.d % 256 == 0 && num_sms >= 2;
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
     a.n_tiles = c.ff / 128;

@@ -59,7 +59,7 @@ def main():
                 ctx.token_init(slots, h0[:n])
                 ctx.enqueue(l, slots, topk_idx=torch.zeros(n, 1, dtype=torch.int32, device="cuda"),
                             topk_w=torch.ones(n, 1, device="cuda"))
-                gb = amoe.GroupBuffers(ctx, ((n + 255) // 256) * 256).set_queues([(l, 0)])
+                gb = amoe.GroupBuffers(ctx, ((n + 255) // 256) * 256).set_queues([(l, 0)], max_rows_hint=n)
                 ctx.rebatch(gb)
                 gbs.append(gb)
             torch.cuda.synchronize()
@@ -103,7 +103,8 @@ def main():
                 for l in range(2):
                     ctx.token_init(slots, h0[:nt])
                     ctx.enqueue(l, slots, topk_idx=idx, topk_w=torch.ones(nt, 1, device="cuda"))
-                    gb = amoe.GroupBuffers(ctx, Gx * ((n + 255) // 256) * 256).set_queues([(l, e) for e in range(Gx)])
+                    gb = amoe.GroupBuffers(ctx, Gx * ((n + 255) // 256) * 256).set_queues(
+                        [(l, e) for e in range(Gx)], max_rows_hint=n)
                     ctx.rebatch(gb)
                     gbs.append(gb)
                 for gb in gbs:
