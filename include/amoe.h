@@ -34,7 +34,10 @@
  *    AMOE_ECUDA ...). Device-side invariant breaches (ring overflow, leg count > K, expert
  *    index out of range, leg for a non-hosted queue) are latched into a device error word and
  *    reported as AMOE_EDEVICE by amoe_check() / amoe_run(); amoe_error_info() gives details.
- *  - Contexts: one per (process, GPU, rank); not thread-safe.
+ *  - Contexts: one per (process, GPU, rank); not thread-safe. Issue a context's launches on one
+ *    stream at a time (its FFN tile-claim counters and group scratch live in the workspace).
+ *  - Launches use programmatic dependent launch (kernel boundaries on a stream overlap the next
+ *    kernel's launch with the previous kernel's tail); AMOE_PDL=0 turns it off.
  *  - Empty work is legal: draining empty queues yields n = 0 and the later calls are no-ops.
  *  - Layouts are row-major; bf16 is IEEE bfloat16 bit patterns (uint16), fp32 is float.
  */
