@@ -538,3 +538,13 @@ def test_open_loop_stepping_and_token_times():
     tt = s["tok_time"].cpu().numpy()
     assert np.all(tt[:, 0] > 0) and np.all(tt[:, 1] > tt[:, 0])
     assert picks >= P.L
+
+
+def test_die_probe_partitions_the_sms():
+    """amoe_die_info: the SM -> die probe either finds no split, or splits every SM of the device
+    into two dies of at least a quarter of the SMs each (B200: 74/74, 72/76 or 70/78 seen)."""
+    from paper_2505_08944_b200 import amoe
+    n0, n1 = amoe.die_info()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert n0 + n1 == sms
+    assert n1 == 0 or (n0 >= sms // 4 and n1 >= sms // 4)
