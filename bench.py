@@ -394,6 +394,7 @@ def main():
         "die_map_sms": list(amoe.die_info()),
         "clocks": clk,
         "stall": {"idle_frac_per_rank": [round(v[0], 4) for v in stall], "layer_barriers": int(stall[0][1]),
+                  "busy_frac_rank0": round(sum(v[0] for v in prof.values()) / ms, 4) if ms else None,
                   "definition": "time a rank's scheduler found no runnable queue / its amoe_run wall time"},
         "roofline": {"bound": "tensor", "kernel": FFN_KERNEL(d),
                      "achieved": gu_tflops, "peak": peak_sust, "unit": "TFLOP/s",
