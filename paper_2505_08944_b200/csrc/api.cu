@@ -655,6 +655,12 @@ amoe_status amoe_get_buffer(amoe_ctx_t c, int which, void** ptr, size_t* bytes) 
   return AMOE_OK;
 }
 
+// published depth (snapshot) of the group's j-th queue
+static int32_t group_rows(const amoe_ctx* c, const amoe_group& g, int j, const uint32_t* Q, int H) {
+  const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
+  return (int32_t)Q[(size_t)g.layer[j] * H + lq];
+}
+
 amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, amoe_run_stats* stats, void* stream) {
   if (!c || !p || p->policy < 0 || p->policy > AMOE_SYNC || p->W < 0) return AMOE_EINVAL;
   for (int r = 0; r < c->cfg.G; ++r)
@@ -690,6 +696,10 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   int idle_streak = 0;
   // AMOE_SYNC: the layer this rank may run, and whether it has arrived at that layer's barrier
   const bool sync = p->policy == AMOE_SYNC;
+  const char* sp_env = getenv("AMOE_SPLIT_PICK");
+  // opt-in: measured slower at every T tried (the second drain + gather + FFN launches cost more
+  // than the cold queues gain on the 1-CTA kernels, profiles/r01_T_sweep.md)
+  const bool split_pick = c->cfg.dtype == AMOE_BF16 && sp_env && sp_env[0] == '1';
   int sync_layer = c->start_layer;
   bool sync_arrived = false;
   // barrier flag value: (run epoch, barrier index + 1), so ranks agree without shared history
@@ -785,15 +795,35 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       // performance hint for the FFN kernel choice: the largest published queue at this pick
       // (a drain takes at least that many; single-rank waves take exactly that many)
       g.max_rows_hint = 0;
-      for (int j = 0; j < g.nq; ++j) {
-        const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
-        g.max_rows_hint = std::max<int32_t>(g.max_rows_hint, (int32_t)Q[(size_t)g.layer[j] * H + lq]);
-      }
+      for (int j = 0; j < g.nq; ++j) g.max_rows_hint = std::max(g.max_rows_hint, group_rows(c, g, j, Q.data(), H));
       const int64_t l0 = c->launches;
-      if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;
+      // AMOE_SPLIT_PICK=1: a pick that mixes cold queues (<= 128 rows: weight-streaming) with hot
+      // ones runs as two launches on the same stream, cold first: the cold part gets the 1-CTA / split-K kernels
+      // instead of padding 256-row pair tiles (profiles/r01_T_sweep.md). Buffers are reused:
+      // the second drain is stream-ordered behind the first group's forward.
+      int n_cold = 0;
+      for (int j = 0; j < g.nq; ++j) n_cold += group_rows(c, g, j, Q.data(), H) <= 128;
+      if (split_pick && n_cold > 0 && n_cold < g.nq) {
+        amoe_group gc = g, gh = g;
+        gc.nq = gh.nq = 0;
+        gc.max_rows_hint = gh.max_rows_hint = 0;
+        for (int j = 0; j < g.nq; ++j) {
+          const int32_t r = group_rows(c, g, j, Q.data(), H);
+          amoe_group& t = r <= 128 ? gc : gh;
+          t.layer[t.nq] = g.layer[j];
+          t.expert[t.nq] = g.expert[j];
+          t.max_rows_hint = std::max(t.max_rows_hint, r);
+          ++t.nq;
+        }
+        if ((st = amoe_rebatch_ffn_forward(c, &gc, 0, s)) != AMOE_OK) return st;
+        if ((st = amoe_rebatch_ffn_forward(c, &gh, 0, s)) != AMOE_OK) return st;
+        rs.picks += 1;   // one pick, two launches
+      } else {
+        if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;
+        rs.picks += 1;
+      }
       if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
       rs.kernel_launches += c->launches - l0;
-      rs.picks += 1;
       rs.queues_run += g.nq;
       idle_streak = 0;
     } else if (cpend > 0) {

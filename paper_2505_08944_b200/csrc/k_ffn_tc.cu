@@ -174,6 +174,32 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 2 loads of 16 columns in flight behind ONE tcgen05.wait::ld (one asm statement, so no use of
+// the outputs can be scheduled above the wait): v[16k + i] = column i at address a{k}.
+__device__ __forceinline__ void tmem_ld16x2(uint32_t a0, uint32_t a1, float* v) {
+  uint32_t r[32];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t" "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(a0), "r"(a1)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 4 loads of 16 columns in flight behind ONE tcgen05.wait::ld (one asm statement, so no use of
+// the outputs can be scheduled above the wait): v[16k + i] = column i at address a{k}.
+__device__ __forceinline__ void tmem_ld16x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, float* v) {
+  uint32_t r[64];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%64];\n\t" "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%65];\n\t" "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%66];\n\t" "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%67];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // ------------------------------------------------------------------ tile schedule
 struct Sched {
   int nq, n_tiles, total, group;
@@ -321,6 +347,12 @@ __device__ __forceinline__ void flush_count(const DevCtx& dc, PendCount& pend, u
 // bf16) first, the accumulator is released to the MMA issuer, and only then do the global
 // stores (and, fused forward, the leg-piece counting) run — off the MMA's critical path.
 // GATEUP: act = bf16(silu(g)·u), 128 columns; DOWN: out / home pool = bf16(v), BN columns.
+#ifndef AMOE_EPI_LD
+#define AMOE_EPI_LD 4
+#endif
+// TMEM loads per tcgen05.wait::ld in the epilogue (2 or 4): each wait is a full TMEM round trip.
+constexpr int EPI_LD = AMOE_EPI_LD;
+
 template <int MODE, int BN, typename Release>
 __device__ __forceinline__ void epilogue_tile(const FfnArgs& args, const DevCtx& dc, uint32_t taddr, bool valid,
                                               __nv_bfloat16* orow, int nb, const amoe_leg& leg, uint32_t stage,
@@ -329,23 +361,33 @@ __device__ __forceinline__ void epilogue_tile(const FfnArgs& args, const DevCtx&
   uint32_t w[NW];
   if (MODE == MODE_GATEUP) {
 #pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-      float g[16], u[16];
-      tmem_ld16(taddr + ch * 16, g);
-      tmem_ld16(taddr + 128 + ch * 16, u);
+    for (int ch = 0; ch < 8; ch += EPI_LD / 2) {
+      float gu[16 * EPI_LD];     // [g(ch), u(ch), g(ch+1), u(ch+1), ...], one wait per batch
+      if constexpr (EPI_LD == 4)
+        tmem_ld16x4(taddr + ch * 16, taddr + 128 + ch * 16, taddr + ch * 16 + 16, taddr + 144 + ch * 16, gu);
+      else
+        tmem_ld16x2(taddr + ch * 16, taddr + 128 + ch * 16, gu);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        __nv_bfloat162 p = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
-        w[ch * 8 + j] = *reinterpret_cast<uint32_t*>(&p);
+      for (int b = 0; b < EPI_LD / 2; ++b) {
+        const float* g = gu + 32 * b;
+        const float* u = g + 16;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 p = __floats2bfloat162_rn(silu_mul(g[2 * j], u[2 * j]), silu_mul(g[2 * j + 1], u[2 * j + 1]));
+          w[(ch + b) * 8 + j] = *reinterpret_cast<uint32_t*>(&p);
+        }
       }
     }
   } else {
 #pragma unroll
-    for (int ch = 0; ch < BN / 16; ++ch) {
-      float v[16];
-      tmem_ld16(taddr + ch * 16, v);
+    for (int ch = 0; ch < BN / 16; ch += EPI_LD) {
+      float v[16 * EPI_LD];
+      if constexpr (EPI_LD == 4)
+        tmem_ld16x4(taddr + ch * 16, taddr + ch * 16 + 16, taddr + ch * 16 + 32, taddr + ch * 16 + 48, v);
+      else
+        tmem_ld16x2(taddr + ch * 16, taddr + ch * 16 + 16, v);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 8 * EPI_LD; ++j) {
         __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
         w[ch * 8 + j] = *reinterpret_cast<uint32_t*>(&p);
       }

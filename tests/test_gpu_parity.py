@@ -233,6 +233,30 @@ def test_shared_experts_and_topk6():
     assert floored_err(to_np(ctx.state()["h"]), ref) <= TOL["bf16"]
 
 
+def test_split_pick_mixed_hot_cold(monkeypatch):
+    """A grouped pick holding hot queues (the shared experts: every token) and cold ones (routed,
+    <= 128 rows) runs as a cold launch (1-CTA kernels) then a hot one (CTA-pair kernels): same
+    tokens as the single launch, within the oracle tolerance, and more launches."""
+    P = Problem(L=2, E=64, K=6, S=2, d=256, ff=512, T=512, seed=11)
+    W, SH = P.oracle_weights()
+    ref, _ = drivers.sync_run(host_values(P.h0[0], "bf16"), P.logits, W, P.K, n_passes=1, shared=SH)
+    launches = {}
+    for sp in ("0", "1"):
+        monkeypatch.setenv("AMOE_SPLIT_PICK", sp)
+        ctx = P.make_ctx()
+        admit(ctx, P)
+        stats = ctx.run(retire_pass=1)
+        torch.cuda.synchronize()
+        ctx.check()
+        assert stats["legs"] == P.T * P.L * (P.K + P.S)
+        h = to_np(ctx.state()["h"])
+        assert floored_err(h, ref) <= TOL["bf16"]
+        assert row_l2_err(h, ref) <= ROW_L2["bf16"] * 2
+        launches[sp] = stats["kernel_launches"] / stats["picks"]
+        ctx.close()
+    assert launches["1"] > launches["0"]
+
+
 @pytest.mark.parametrize("E,K,S,T,cap", [
     (1, 1, 0, 300, 0),      # one expert, top-1: the layer is a dense SwiGLU MLP
     (4, 4, 0, 257, 0),      # K = E: every token visits every expert (ragged T)

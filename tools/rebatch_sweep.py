@@ -19,7 +19,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 NS = sorted({1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 192, 256, 320, 384, 512, 1024, 2048, 4096})
-SHAPES = {"mixtral": (4096, 14336, 4), "deepseek": (2048, 1408, 32)}
+SHAPES = {"mixtral": (4096, 14336, 4), "deepseek": (2048, 1408, 32),
+          # diagnostics: the DeepSeek width with 2x / 4x the FFN width (longer K in the down GEMM)
+          "deepseek_ff2x": (2048, 2816, 16), "deepseek_ff4x": (2048, 5632, 8)}
 
 
 def main():
