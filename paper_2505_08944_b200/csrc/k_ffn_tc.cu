@@ -766,10 +766,20 @@ struct Sched2 {
   }
 };
 
+#ifdef AMOE_TRACE
+// diagnostic build only (-DAMOE_TRACE): per-CTA timeline of the last launch of each mode,
+// read with amoe_debug_ffn_trace (tools/ffn_trace.py)
+__device__ unsigned long long g_ffn_trace[2][8][160];
+#define FFN_TRACE(i, v) (g_ffn_trace[MODE == MODE_GATEUP ? 0 : 1][i][blockIdx.x] = (v))
+#else
+#define FFN_TRACE(i, v) ((void)0)
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1)
 ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, const __grid_constant__ DevCtx dc) {
   AMOE_PDL_ENTRY();
+  if (threadIdx.x == 0) FFN_TRACE(0, globaltimer_ns());
   __shared__ unsigned long long s_fwd[2];
   __shared__ int4 s_epi_rec[1];            // die schedule: the epilogue's current unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -846,6 +856,7 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (tid == 0) FFN_TRACE(1, globaltimer_ns());
   Sched2 sc{nq, args.n_tiles, s_pre[nq], args.group_m, s_n, s_pre};
   const int kb_n = args.k_blocks;
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -1016,16 +1027,40 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     constexpr uint32_t idesc = idesc_bf16(BM2, 256);
     int stage = 0; uint32_t phase = 0;
     int acc = 0; uint32_t acc_phase = 0;
+#ifdef AMOE_TRACE
+    unsigned long long t_wait_full = 0, t_wait_tmem = 0, t_ring = 0;
+#endif
     for (int it = 0;; ++it) {
+#ifdef AMOE_TRACE
+      const unsigned long long tr0 = globaltimer_ns();
+#endif
       const int4 U = die_sched ? ring_get(it) : static_unit(it);
+#ifdef AMOE_TRACE
+      t_ring += globaltimer_ns() - tr0;
+      if (U.x < 0) { FFN_TRACE(3, globaltimer_ns()); FFN_TRACE(4, it); FFN_TRACE(5, t_wait_full); FFN_TRACE(6, t_wait_tmem); FFN_TRACE(7, t_ring); }
+#endif
       if (U.x < 0) break;
       const int ks = U.w;
       const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
+#ifdef AMOE_TRACE
+      const unsigned long long tt0 = globaltimer_ns();
+#endif
       mbar_wait(smem_u32(&bars[2 * STAGES2 + 2 + acc]), acc_phase ^ 1u);
+#ifdef AMOE_TRACE
+      t_wait_tmem += globaltimer_ns() - tt0;
+#endif
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
       for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef AMOE_TRACE
+        const unsigned long long tf0 = globaltimer_ns();
+#endif
         mbar_wait(smem_u32(&bars[stage]), phase);
+#ifdef AMOE_TRACE
+        const unsigned long long tf1 = globaltimer_ns();
+        t_wait_full += tf1 - tf0;
+        if (it == 0 && kb == kb0) FFN_TRACE(2, tf1);
+#endif
         tc_fence_after();
         const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
         const uint64_t adesc = umma_desc_sw128(sa);
@@ -1098,6 +1133,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   __syncthreads();
   cluster_sync();
   tc_fence_after();
+#ifdef AMOE_TRACE
+  if (tid == 0 && !leader) FFN_TRACE(3, globaltimer_ns());   // follower CTA: end time in slot 3
+#endif
   if (MODE == MODE_DOWN && args.fuse && tid == 0) {
     unsigned long long* st = wsp<unsigned long long>(dc, dc.rank, dc.lay.stats);
     if (s_fwd[0]) atomicAdd(st + 2, s_fwd[0]);
@@ -1285,6 +1323,16 @@ __global__ void die_probe_kernel(const uint32_t* buf, uint32_t* lat, int* smids)
 
 int die_map(uint64_t mask[4], int counts[2]);
 }  // namespace amoe
+
+#ifdef AMOE_TRACE
+// [mode][slot][cta]: 0 entry, 1 setup done, 2 first stage full (leader), 3 MMA done (leader) /
+// pair end (follower), 4 units (leader), 5/6/7 MMA issuer's ns waiting on full stages / TMEM /
+// the unit ring (leader)
+extern "C" amoe_status amoe_debug_ffn_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, amoe::tc::tc2::g_ffn_trace, sizeof(amoe::tc::tc2::g_ffn_trace)) == cudaSuccess ? AMOE_OK
+                                                                                                    : AMOE_ECUDA;
+}
+#endif
 
 extern "C" amoe_status amoe_die_info(int32_t counts[2]) {
   if (!counts) return AMOE_EINVAL;
