@@ -672,7 +672,16 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 // Per CTA and per K=16 step this stages 8 KB instead of 12 KB (-33 % L2->SM bytes per FLOP).
 namespace tc2 {
 using namespace tc;
-constexpr int STAGES2 = 6;
+#ifndef AMOE_STAGES2
+#define AMOE_STAGES2 6
+#endif
+#ifndef AMOE_L2PF
+#define AMOE_L2PF 0
+#endif
+constexpr int STAGES2 = AMOE_STAGES2;
+// producer L2 prefetch distance in K blocks (0: off): the first CTA to touch an operand line
+// pays the DRAM latency; a bulk-tensor L2 prefetch that many blocks ahead hides it
+constexpr int L2PF = AMOE_L2PF;
 constexpr int HALF_BYTES = 128 * BK * 2;                     // 16 KB
 constexpr int STAGE2_BYTES = 2 * HALF_BYTES;                 // A half + B half = 32 KB
 constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + 4096 + EPI_STAGE_BYTES + 1024;
@@ -696,6 +705,9 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap,
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2(const void* tmap, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" :: "l"(tmap), "r"(c0), "r"(c1) : "memory");
 }
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -1018,6 +1030,10 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
         if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * STAGE2_BYTES);
         tma_load_2d_pair(sa, &tmA, kb * BK, arow, full_leader);
         tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
+        if (L2PF > 0 && kb + L2PF < kb1) {
+          tma_prefetch_l2(&tmA, (kb + L2PF) * BK, arow);
+          tma_prefetch_l2(bmap, (kb + L2PF) * BK, brow);
+        }
         if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
         if (kb == kb0 && die_sched && leader) advance(it);
       }
@@ -1440,6 +1456,9 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
                   void* act, void* out, const amoe_leg* meta, int fuse, int gathered, int num_sms, cudaStream_t s,
                   int part) {
   using namespace tc;
+#ifdef AMOE_TRACE
+  if (const char* g = getenv("AMOE_TRACE_GRID")) num_sms = std::min(num_sms, atoi(g));   // diagnostic
+#endif
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_GATEUP, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);

@@ -55,12 +55,13 @@ def main():
     res = {"shape": args.shape, "n": n, "event_us_both": e0.elapsed_time(e1) * 1e3}
     for mi, mode in enumerate(("gateup", "down")):
         t = buf[mi].astype(np.int64)
-        ncta = 148
+        ncta = int((t[0] > 0).sum())          # CTAs launched (AMOE_TRACE_GRID may shrink the grid)
         t0 = t[0, :ncta].min()
         lead = np.arange(0, ncta, 2)
         foll = lead + 1
         end = t[3, foll]
         r = {
+            "ctas": ncta,
             "span_us": float((end.max() - t0) / 1e3),
             "entry_spread_us": float((t[0, :ncta].max() - t0) / 1e3),
             "setup_us_median": float(np.median(t[1, :ncta] - t[0, :ncta]) / 1e3),
