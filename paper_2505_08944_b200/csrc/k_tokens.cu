@@ -10,7 +10,10 @@ namespace amoe {
 
 constexpr int kTokThreads = 256;
 constexpr int kTokWarps = kTokThreads / kWarp;
-constexpr int kTPW = 4;                       // tokens per warp per chunk
+#ifndef AMOE_TPW
+#define AMOE_TPW 4
+#endif
+constexpr int kTPW = AMOE_TPW;                // tokens per warp per chunk
 constexpr int kTPC = kTokWarps * kTPW;        // tokens per CTA chunk
 // 16-byte chunks per lane batched in the merge. 1 keeps the kernel at ~48 registers (~40 resident
 // warps/SM); measured on B200: kU = 4 (128 regs) and kU = 2 with a register cap (spills) were
