@@ -164,7 +164,10 @@ amoe_status amoe_create(const amoe_config* cfg, void* workspace, size_t bytes, a
  * process: opened CUDA IPC handles / symm_mem buffer_ptrs, or local aliases for loopback tests).
  * peer_ws[rank] must equal this context's workspace. Setup only. The caller must synchronise all
  * ranks (device sync + process barrier) after every rank's amoe_create and before the first
- * amoe_enqueue anywhere: amoe_create zeroes the rings that peers push legs into. */
+ * amoe_enqueue anywhere: amoe_create zeroes the rings that peers push legs into. Workspaces on
+ * other devices get peer access enabled from the current device (cudaDeviceEnablePeerAccess).
+ * Errors: AMOE_EPEER if an address is null, unaligned, not a device address, or on a device
+ * this one cannot reach as a peer. */
 amoe_status amoe_import_peers(amoe_ctx_t ctx, const uint64_t* peer_ws, int G);
 
 /* Register expert weights of (layer, expert) hosted here (expert >= E: shared expert

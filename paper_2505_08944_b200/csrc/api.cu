@@ -291,10 +291,29 @@ amoe_status amoe_create(const amoe_config* cfg, void* workspace, size_t bytes, a
 amoe_status amoe_import_peers(amoe_ctx_t c, const uint64_t* peer_ws, int G) {
   if (!c || !peer_ws || G != c->cfg.G) return AMOE_EINVAL;
   if (peer_ws[c->cfg.rank] != reinterpret_cast<uint64_t>(c->ws)) return AMOE_EPEER;
-  for (int r = 0; r < G; ++r) {
+  for (int r = 0; r < G; ++r)
     if (!peer_ws[r] || (peer_ws[r] & 255)) return AMOE_EPEER;
-    c->dc.peer[r] = peer_ws[r];
+  // kernels of this device dereference every peer workspace (one-sided legs over NVLink): a
+  // workspace that lives on another device needs peer access from this one. An IPC handle
+  // opened under the peer's device guard does not grant it, so enable it here (idempotent).
+  int me = -1;
+  CK(cudaGetDevice(&me));
+  for (int r = 0; r < G; ++r) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, reinterpret_cast<const void*>(peer_ws[r])) != cudaSuccess) {
+      cudaGetLastError();
+      return AMOE_EPEER;              // not a device address in this process
+    }
+    if (a.type == cudaMemoryTypeDevice && a.device >= 0 && a.device != me) {
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, me, a.device));
+      if (!can) return AMOE_EPEER;
+      const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return AMOE_ECUDA;
+    }
   }
+  for (int r = 0; r < G; ++r) c->dc.peer[r] = peer_ws[r];
   return AMOE_OK;
 }
 
