@@ -241,10 +241,18 @@ def main():
 
     G, rank, local = D.env()
     assert G == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {G}"
+    # AMOE_DIST_BACKEND=gloo: ranks may share a GPU (local rank mod device count) — the N > 1
+    # path exercised on a one-GPU box; the data path is the same (peer workspaces via IPC)
+    backend = os.environ.get("AMOE_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if G > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else "cpu"       # device of the timing / stall reductions
     spec = wl.CONFIGS[args.config]
     L = args.L or spec.L
     T = args.T or spec.T
@@ -334,8 +342,8 @@ def main():
     legs = sum(r["legs"] for r in runs)
     # per-GPU stall: host wall time of scheduler polls that found nothing of this rank's to run
     stall = D.gather_values([sum(r["idle_ns"] for r in runs) / max(1, sum(r["wall_ns"] for r in runs)),
-                             sum(r["barriers"] for r in runs)], device=dev)
-    ms, (token_layers, legs) = D.reduce_timing(ms, [token_layers, legs], device=dev)
+                             sum(r["barriers"] for r in runs)], device=cdev)
+    ms, (token_layers, legs) = D.reduce_timing(ms, [token_layers, legs], device=cdev)
     assert token_layers == G * T * L * args.steps, (token_layers, G * T * L * args.steps)
     value = token_layers / (ms / 1e3)
 
@@ -371,7 +379,7 @@ def main():
     t_exec = sum(max(6.0 * d * ff * n / f_pk, (6.0 * d * ff + 4.0 * n * d) / bw) for _, _, n in execs)
     t_act = my_tl * ((K + S) * d * 2 + 3 * d * 2 + E * 4) / bw
     t_ideal = 6.0 * d * ff * my_legs / f_pk
-    per_rank = D.gather_values([1e3 * (t_exec + t_act), 1e3 * t_ideal], device=dev)
+    per_rank = D.gather_values([1e3 * (t_exec + t_act), 1e3 * t_ideal], device=cdev)
     t_roof_ms = max(v[0] for v in per_rank)
     t_ideal_ms = max(v[1] for v in per_rank)
     hist = {}
@@ -427,7 +435,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ems, _ = D.reduce_timing(e0.elapsed_time(e1), [], device=dev)
+        ems, _ = D.reduce_timing(e0.elapsed_time(e1), [], device=cdev)
         line["e2e"] = {"value": G * T * L * args.steps / (ems / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": int(h0_host.numel() * 2 + rt_host[0].numel() * 4),
                        "d2h_bytes_per_step": int(hout.numel() * 2),
