@@ -253,6 +253,12 @@ amoe_status amoe_create(const amoe_config* cfg, void* workspace, size_t bytes, a
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  // AMOE_NUM_SMS: persistent grids of this context sized for fewer SMs (contexts of one process
+  // co-running on disjoint halves of a GPU emulate G GPUs: tools/g_emulate.py)
+  if (const char* e = getenv("AMOE_NUM_SMS")) {
+    const int n = atoi(e);
+    if (n >= 2 && n < c->num_sms) c->num_sms = n & ~1;
+  }
   DevCtx& d = c->dc;
   memset(&d, 0, sizeof(d));
   d.L = cfg->L; d.E = cfg->E; d.K = cfg->K; d.S = cfg->S; d.d = cfg->d; d.ff = cfg->ff;
