@@ -353,16 +353,22 @@ def test_loopback_peers_match_single_gpu(G):
     assert remote > 0
 
 
-@pytest.mark.parametrize("G,d,policy", [(2, 128, "defrag"), (4, 256, "defrag"), (2, 128, "sync"), (4, 256, "sync")])
-def test_loopback_amoe_run_concurrent_ranks(G, d, policy):
+@pytest.mark.parametrize("G,d,policy,sms", [(2, 128, "defrag", 0), (4, 256, "defrag", 0), (2, 128, "sync", 0),
+                                             (4, 256, "sync", 0), (2, 256, "defrag", 74), (4, 256, "flfs", 36)])
+def test_loopback_amoe_run_concurrent_ranks(G, d, policy, sms, monkeypatch):
     """The native multi-rank loop: G contexts on one GPU, each running amoe_run in its own host
     thread on its own CUDA stream, concurrently. Legs cross ranks through peer rings (remote
     reservations race with local producers), outputs return by one-sided stores, and each rank
-    keeps serving until every rank's done flag is set. Result: bit-identical to one rank."""
+    keeps serving until every rank's done flag is set. Result: bit-identical to one rank.
+    sms > 0: each context's persistent grids sized for that many SMs (AMOE_NUM_SMS, the
+    tools/g_emulate.py setup: ranks co-running on SM slices of one GPU)."""
     import threading
     T = 128
     P = Problem(L=2, E=8, K=2, S=0, d=d, ff=256, T=T, G=G, seed=14)
+    if sms:
+        monkeypatch.setenv("AMOE_NUM_SMS", str(sms))
     ctxs = [P.make_ctx(rank=r) for r in range(G)]
+    monkeypatch.delenv("AMOE_NUM_SMS", raising=False)
     ptrs = [c.ws.data_ptr() for c in ctxs]
     for c in ctxs:
         c.import_peers(ptrs)
