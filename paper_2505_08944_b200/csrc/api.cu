@@ -721,6 +721,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   int idle_streak = 0;
   // AMOE_SYNC: the layer this rank may run, and whether it has arrived at that layer's barrier
   const bool sync = p->policy == AMOE_SYNC;
+  // G > 1, asynchronous policies: pending merges run before the next pick (AMOE_COMBINE_FIRST=0
+  // restores pick-first). Measured on the G-rank emulation: 10-28 % fewer executions, +2-8 %
+  // throughput (profiles/r01_g_emulate.md)
+  const char* cf_env = getenv("AMOE_COMBINE_FIRST");
+  const bool combine_first = c->cfg.G > 1 && !sync && p->max_picks == 0 && !(cf_env && cf_env[0] == '0');
   const char* sp_env = getenv("AMOE_SPLIT_PICK");
   // opt-in: measured slower at every T tried (the second drain + gather + FFN launches cost more
   // than the cold queues gain on the 1-CTA kernels, profiles/r01_T_sweep.md)
@@ -794,6 +799,15 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         if (bb != sync_layer) std::fill(Q.begin() + (size_t)bb * H, Q.begin() + (size_t)(bb + 1) * H, 0u);
     const uint32_t* cc = reinterpret_cast<const uint32_t*>(snap + c->lay.cctr);
     const uint32_t cpend = cc[1] - cc[2];
+    if (combine_first && cpend > 0) {
+      // merge the tokens whose last legs arrived from other ranks before picking: their next
+      // layer's legs join the queues first, so the pick drains one batch instead of a fragment
+      const int64_t l0 = c->launches;
+      if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
+      rs.kernel_launches += c->launches - l0;
+      idle_streak = 0;
+      continue;
+    }
     int b = -1, q = -1;
     const int pol = sync ? AMOE_MTFS : p->policy;
     const bool work = pick_queue(Q.data(), L, H, c->cfg.E + c->cfg.S, pol, p->W, (double)p->delta, &b, &q) == 0;
