@@ -144,8 +144,10 @@ typedef struct amoe_run_stats {
   int64_t token_layers;    /* merges completed on this rank (homed tokens) */
   int64_t kernel_launches; /* libamoe kernels launched */
   int64_t idle_polls;      /* scheduler polls that found nothing to run */
-  int64_t idle_ns;         /* host wall time of those polls: the GPU had nothing of this rank's
-                              queues to run (each poll synchronises the stream first) = stall */
+  int64_t idle_ns;         /* host wall time of those polls, counted from the moment the poll's
+                              stream synchronisation returned (this rank's earlier kernels done)
+                              to the next poll: the GPU had nothing of this rank's queues to run
+                              = stall (includes AMOE_GROW_WAIT deferrals) */
   int64_t wall_ns;         /* host wall time of the whole amoe_run call */
   int64_t barriers;        /* AMOE_SYNC: layer barriers passed */
 } amoe_run_stats;
