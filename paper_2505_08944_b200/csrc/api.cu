@@ -728,9 +728,9 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   const bool combine_first = c->cfg.G > 1 && !sync && p->max_picks == 0 && !(cf_env && cf_env[0] == '0');
   // G > 1, asynchronous policies: defer a pick while the picked layer's hosted depth is still
   // growing between polls (legs streaming in from a peer's merge), at most AMOE_GROW_WAIT us
-  // per layer (default 100; 0 disables). Measured on the G-rank emulation: 20-40 % fewer
+  // per layer (default 200; 0 disables). Measured on the G-rank emulation: 20-40 % fewer
   // executions, +2-8 % throughput (profiles/r01_g_emulate.md). The wait counts as idle time.
-  int64_t grow_ns = 100000;
+  int64_t grow_ns = 200000;
   if (const char* ge = getenv("AMOE_GROW_WAIT")) grow_ns = (int64_t)(atof(ge) * 1e3);
   if (c->cfg.G == 1 || sync || p->max_picks > 0) grow_ns = 0;
   std::vector<uint64_t> prev_depth(grow_ns > 0 ? c->cfg.L : 0, 0);
