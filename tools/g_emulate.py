@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--skew", default="zipf", help="router skew: zipf (s from the config) or exp")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     import torch
@@ -62,7 +63,8 @@ def main():
                 c.set_expert(l, e, *w)
                 keep.append(w)
         tab = torch.from_numpy(np.stack([wl.router_logits(args.seed, L, T, E, zipf_s=spec.zipf_s, pass_idx=p,
-                                                          token_offset=r * T) for p in range(2)])).to(dev)
+                                                          token_offset=r * T, skew=args.skew)
+                                          for p in range(2)])).to(dev)
         c.set_router(tab)
         tables.append(tab)
         h0s.append(torch.from_numpy(wl.hidden0(args.seed, T, d, token_offset=r * T).view(np.int16)).view(
@@ -113,7 +115,7 @@ def main():
     tl = sum(s["token_layers"] for st in runs for s in st)
     assert tl == G * T * L * args.steps, (tl, G * T * L * args.steps)
     idle = [sum(st[r]["idle_ns"] for st in runs) / max(1, sum(st[r]["wall_ns"] for st in runs)) for r in range(G)]
-    line = {"tool": "g_emulate", "config": args.config, "policy": args.policy, "W": args.W, "delta": args.delta, "G": G,
+    line = {"tool": "g_emulate", "config": args.config, "policy": args.policy, "skew": args.skew, "W": args.W, "delta": args.delta, "G": G,
             "sms_per_rank": int(os.environ["AMOE_NUM_SMS"]), "L": L, "T_per_rank": T, "steps": args.steps,
             "value": tl / total, "unit": "token-layers/s (host wall, device-synced)",
             "ms_per_step": 1e3 * total / args.steps, "idle_frac_per_rank": [round(x, 4) for x in idle],
