@@ -721,16 +721,20 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   int idle_streak = 0;
   // AMOE_SYNC: the layer this rank may run, and whether it has arrived at that layer's barrier
   const bool sync = p->policy == AMOE_SYNC;
-  // G > 1, asynchronous policies: pending merges run before the next pick (AMOE_COMBINE_FIRST=0
-  // restores pick-first). Measured on the G-rank emulation: 10-28 % fewer executions, +2-8 %
-  // throughput (profiles/r01_g_emulate.md)
+  // G > 1, asynchronous policies, ranks hosting >= 2 routed experts (a grouped pick has
+  // something to consolidate), two changes to what the scheduler sees when the GPU goes idle:
+  // - merge first: pending merges (tokens whose last legs came back from other ranks) run
+  //   before the next pick, so their next-layer legs join it (AMOE_COMBINE_FIRST=1/0 forces);
+  // - grow wait: a pick is deferred while its layer's hosted depth still grows between polls
+  //   (legs streaming in from a peer's merge), at most AMOE_GROW_WAIT us (default 200; 0 off).
+  // G-rank emulation (profiles/r01_g_emulate.md): +3-23 % with 4-32 experts per rank, neutral
+  // with 2; with ONE expert per rank (Mixtral at G = 8) both slow the hot expert's rank, which
+  // is everyone's critical path (-12 %), so they stay off there. Deferrals count as idle.
+  const bool multi_expert = c->Hr >= 2;
   const char* cf_env = getenv("AMOE_COMBINE_FIRST");
-  const bool combine_first = c->cfg.G > 1 && !sync && p->max_picks == 0 && !(cf_env && cf_env[0] == '0');
-  // G > 1, asynchronous policies: defer a pick while the picked layer's hosted depth is still
-  // growing between polls (legs streaming in from a peer's merge), at most AMOE_GROW_WAIT us
-  // per layer (default 200; 0 disables). Measured on the G-rank emulation: 20-40 % fewer
-  // executions, +2-8 % throughput (profiles/r01_g_emulate.md). The wait counts as idle time.
-  int64_t grow_ns = 200000;
+  const bool combine_first = c->cfg.G > 1 && !sync && p->max_picks == 0 &&
+                             (cf_env ? cf_env[0] == '1' : multi_expert);
+  int64_t grow_ns = multi_expert ? 200000 : 0;
   if (const char* ge = getenv("AMOE_GROW_WAIT")) grow_ns = (int64_t)(atof(ge) * 1e3);
   if (c->cfg.G == 1 || sync || p->max_picks > 0) grow_ns = 0;
   std::vector<uint64_t> prev_depth(grow_ns > 0 ? c->cfg.L : 0, 0);
