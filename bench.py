@@ -168,17 +168,46 @@ def _oracle_inputs(spec, seed, max_tokens):
     return _ORACLE_INPUTS[key]
 
 
-def cpu_oracle_sample(spec, seed, budget_s=15.0, max_tokens=4096):
-    """Time the oracle (as it stands) on a bounded sample of the same workload: batches of
-    tokens through layer 0 of the configuration (routing, SwiGLU experts, combine, RMSNorm)."""
-    from oracle import numerics as nx
+def host_info():
+    """The host the oracle ran on: CPU model, affinity cores, BLAS library and its threads."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        for r in threadpool_info():
+            if r.get("user_api") == "blas":
+                blas = {"library": r.get("internal_api"), "version": r.get("version"),
+                        "threads": r.get("num_threads"), "arch": r.get("architecture")}
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "affinity_cores": len(os.sched_getaffinity(0)), "blas": blas}
+
+
+def _limits(n):
     try:
         from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
     except Exception:  # pragma: no cover
-        threadpool_limits = None
-    cores = len(os.sched_getaffinity(0))
+        return None
+
+
+def cpu_oracle_sample(spec, seed, budget_s=15.0, max_tokens=4096, threads=None):
+    """Time the oracle (as it stands) on a bounded sample of the same workload: batches of
+    tokens through layer 0 of the configuration (routing, SwiGLU experts, combine, RMSNorm).
+    BLAS threads = the affinity cores (set explicitly, OpenBLAS oversubscribes
+    by default)."""
+    from oracle import numerics as nx
+    cores = threads or len(os.sched_getaffinity(0))
     W, SH, z, h = _oracle_inputs(spec, seed, max_tokens)
-    ctxm = threadpool_limits(limits=cores) if threadpool_limits else None
+    ctxm = _limits(cores)
     try:
         done, t0, batch = 0, time.perf_counter(), 64 if spec.d >= 2048 else 512
         while done < h.shape[0]:
@@ -191,9 +220,38 @@ def cpu_oracle_sample(spec, seed, budget_s=15.0, max_tokens=4096):
     finally:
         if ctxm is not None:
             ctxm.__exit__(None, None, None)
-    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": done / el, "unit": UNIT, "cores": cores, "threads": cores, "kind": "oracle",
             "sample": f"{done} tokens x layer 0 of the {spec.name} config (numpy float64 GEMMs, bf16 "
                       f"rounding), {el:.1f} s"}
+
+
+def cpu_oracle_tiny_e2e(seed):
+    """BASELINE.md §3's tiny-config oracle runs, end to end: the synchronous driver (fixed-batch
+    EP) and the asynchronous µ-queue driver (Algorithm 1 over random interleavings), one pass of
+    all 512 tokens through both layers, single BLAS thread (tiny GEMMs oversubscribe otherwise)."""
+    import workload as wl
+    from oracle import drivers
+    spec = wl.CONFIGS["tiny"]
+    W = [[tuple(wl.f32_from_bf16_bits(a) for a in wl.expert_weights(seed, l, e, spec.d, spec.ff))
+          for e in range(spec.E)] for l in range(spec.L)]
+    tab = wl.router_logits(seed, spec.L, spec.T, spec.E)
+    h0 = wl.f32_from_bf16_bits(wl.hidden0(seed, spec.T, spec.d))
+    out = {}
+    ctxm = _limits(1)
+    try:
+        for name in ("sync", "async"):
+            t0 = time.perf_counter()
+            if name == "sync":
+                drivers.sync_run(h0, lambda p, l: tab[l], W, spec.K, n_passes=1)
+            else:
+                drivers.async_run(h0, lambda p, l: tab[l], W, spec.K, G=1, T=spec.T, n_passes=1, seed=seed)
+            el = time.perf_counter() - t0
+            out[name] = {"value": spec.T * spec.L / el, "unit": UNIT, "threads": 1,
+                         "sample": f"tiny config, {spec.T} tokens x {spec.L} layers, {el:.2f} s"}
+    finally:
+        if ctxm is not None:
+            ctxm.__exit__(None, None, None)
+    return out
 
 
 def run_reference(args):
@@ -219,7 +277,7 @@ def run_reference(args):
             "data": "synthetic (seeded workload generator)",
             "config": config_dict(spec, spec.L, spec.T, args.gpus, args.policy, not args.ungrouped),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": "oracle",
-                             "sample": r["sample"]},
+                             "sample": r["sample"], "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -443,7 +501,19 @@ def main():
 
     # ------------------------------------------------------------------ CPU oracle baseline
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_oracle_sample(spec, args.seed)
+        cb = cpu_oracle_sample(spec, args.seed)
+        cb["host"] = host_info()
+        # BASELINE.md §3's other oracle samples, reported beside the headline one
+        extra = {}
+        try:
+            extra["tiny_e2e"] = cpu_oracle_tiny_e2e(args.seed)
+            other = "deepseek" if spec.name == "mixtral" else "mixtral"
+            ds = cpu_oracle_sample(wl.CONFIGS[other], args.seed, budget_s=6.0, max_tokens=2048)
+            extra[f"{other}_layer0"] = ds
+        except Exception as e:  # pragma: no cover - reported, never fatal
+            extra["error"] = repr(e)
+        cb["other_samples"] = extra
+        line["cpu_baseline"] = cb
 
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -211,7 +211,9 @@ amoe_status amoe_enqueue(amoe_ctx_t ctx, int layer, const int32_t* slots, int T,
 amoe_status amoe_queue_depths(amoe_ctx_t ctx, uint32_t* host_out, void* stream);
 
 /* Algorithm 1 / MTFS / FLFS over a host snapshot Q [L * H] (W = lookahead depth, δ = decay;
- * divisor = E, reading c11; ties to the smallest (layer, queue)). AMOE_IDLE when all empty. */
+ * the lookahead divisor N_E is the block's expert count E + S, routed plus shared, box-wide —
+ * DESIGN.md reading c11; ties to the smallest (layer, queue)). AMOE_IDLE when all empty.
+ * AMOE_DEFRAG_GLOBAL is not accepted here (it needs the peers' counters: amoe_run only). */
 amoe_status amoe_pick(amoe_ctx_t ctx, const uint32_t* Q, int policy, int W, float delta, int* layer,
                       int* queue);
 

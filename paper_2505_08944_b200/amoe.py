@@ -20,7 +20,8 @@ BUF = dict(h=0, x=1, pool=2, tok_w=3, tok_idx=4, tok_layer=5, tok_pass=6, rings=
 STATUS = {0: "OK", 1: "IDLE", 2: "EINVAL", 3: "ENOTHOSTED", 4: "ECUDA", 5: "EDEVICE", 6: "EPEER", 7: "ENOMEM"}
 FAULTS = {1: "ring overflow", 2: "leg count > K+S", 3: "expert index out of range", 4: "not hosted",
           5: "combine ring overflow", 6: "token slot out of range", 7: "stale/unpublished ring entry",
-          8: "no router table"}
+          8: "no router table", 9: "aborted by a peer rank's fault", 10: "amoe_run timeout (G > 1)",
+          11: "lost leg: stranded token"}
 
 # AMOE_LIB: load another build of the same library (A/B measurements of two builds in one run)
 LIB_PATH = os.environ.get("AMOE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libamoe.so")
@@ -216,13 +217,21 @@ class Context:
             raise AmoeError(2, "amoe_workspace_bytes (invalid config)")
         if workspace is None:
             workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        if workspace.dtype != torch.uint8 or not workspace.is_contiguous() or workspace.device.type != "cuda":
+            raise AmoeError(2, "workspace must be a contiguous uint8 CUDA tensor")
         base = workspace.data_ptr()
         pad = (-base) % 256
+        if workspace.numel() - pad < nbytes:
+            # a short buffer would be silently truncated by the slice below; the library's own
+            # size check (AMOE_ENOMEM) only sees the byte count passed to amoe_create
+            raise AmoeError(7, f"workspace holds {workspace.numel() - pad} usable bytes after 256-B alignment, "
+                               f"amoe_workspace_bytes = {nbytes}")
         self.ws_tensor = workspace
         self.ws = workspace[pad:pad + nbytes]
         self.ws_bytes = nbytes
         h = C.c_void_p()
-        self._chk(self.lib.amoe_create(C.byref(cfg), C.c_void_p(self.ws.data_ptr()), nbytes, C.byref(h)), "amoe_create")
+        self._chk(self.lib.amoe_create(C.byref(cfg), C.c_void_p(self.ws.data_ptr()), self.ws.numel(), C.byref(h)),
+                  "amoe_create")
         self.h = h
         self.L, self.E, self.K, self.S, self.d, self.ff = cfg.L, cfg.E, cfg.K, cfg.S, cfg.d, cfg.ff
         self.T, self.G, self.rank = cfg.T_slots, cfg.G, cfg.rank

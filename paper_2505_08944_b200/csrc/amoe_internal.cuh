@@ -28,7 +28,12 @@ enum Fault : uint32_t {
   F_SLOT_RANGE = 6,       // args: slot, T
   F_STALE_ENTRY = 7,      // args: queue, position, seq
   F_NO_ROUTER = 8,        // args: slot, layer, pass (needs amoe_set_router or amoe_set_gate)
+  F_PEER_ABORT = 9,       // args: peer rank whose fault (or timeout) aborted this rank's amoe_run (host-latched)
+  F_RUN_TIMEOUT = 10,     // args: seconds, merged, expected (host-latched: AMOE_RUN_TIMEOUT expired, G > 1)
+  F_LOST_LEG = 11,        // args: stranded token slot, its layer, leg pieces returned (host-latched, G == 1)
 };
+// done[] value a faulting rank stores into every peer: never equal to a run epoch
+constexpr uint32_t kAbortEpoch = 0xFFFFFFFFu;
 
 // Byte offsets of every object inside a rank's workspace. Identical on every rank (the
 // layout depends only on the config), so a peer object's address is peer_base + offset.

@@ -16,7 +16,7 @@ namespace amoe {
 // kernels (k_*.cu)
 int launch_token_init(const DevCtx&, const int32_t*, int, const void*, int, cudaStream_t);
 int launch_enqueue(const DevCtx&, int, const int32_t*, int, const float*, const int32_t*, const float*, cudaStream_t);
-int launch_combine(const DevCtx&, int, cudaStream_t);
+int launch_combine(const DevCtx&, int, int, cudaStream_t);
 int launch_announce(const DevCtx&, uint32_t, int, cudaStream_t);
 int die_map(uint64_t mask[4], int counts[2]);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
@@ -616,7 +616,7 @@ amoe_status amoe_combine(amoe_ctx_t c, int retire_pass, void* stream) {
   DevCtx dc = c->dc;
   if (!dc.router) { dc.n_tab = 1; }
   StageTimer tm(c, ST_COMBINE, s);
-  c->launches += launch_combine(dc, retire_pass, s);
+  c->launches += launch_combine(dc, retire_pass, c->num_sms, s);
   c->last_stream = s;
   CK(cudaGetLastError());
   return AMOE_OK;
@@ -653,6 +653,8 @@ amoe_status amoe_clear_error(amoe_ctx_t c) {
   if (!c) return AMOE_EINVAL;
   CK(cudaDeviceSynchronize());
   CK(cudaMemset(c->ws + c->lay.err, 0, 16));
+  // abort marks peers stored into this rank's done[] slots (multi-GPU fault propagation)
+  CK(cudaMemset(c->ws + c->lay.done, 0, 64));
   return AMOE_OK;
 }
 
@@ -678,6 +680,16 @@ amoe_status amoe_get_buffer(amoe_ctx_t c, int which, void** ptr, size_t* bytes) 
   *ptr = c->ws + off;
   *bytes = n;
   return AMOE_OK;
+}
+
+// Latch a host-detected fault into the device error word (first fault wins, as on the device).
+static void host_latch(amoe_ctx* c, uint32_t code, uint32_t a0, uint32_t a1, uint32_t a2, cudaStream_t s) {
+  uint32_t cur = 0;
+  cudaStreamSynchronize(s);
+  cudaMemcpy(&cur, c->ws + c->lay.err, 4, cudaMemcpyDeviceToHost);
+  if (cur) return;
+  const uint32_t v[4] = {code, a0, a1, a2};
+  cudaMemcpy(c->ws + c->lay.err, v, 16, cudaMemcpyHostToDevice);
 }
 
 // published depth (snapshot) of the group's j-th queue
@@ -758,13 +770,39 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   // nothing is runnable — the caller admits arrivals in between (open-loop serving); no
   // quiescence protocol, no lost-leg verdict
   const bool stepping = p->max_picks > 0;
-  if (stepping && c->cfg.G > 1) return AMOE_EINVAL;
+  // stepping has no layer barrier (the lockstep layer would never advance): AMOE_SYNC is closed-loop only
+  if (stepping && (c->cfg.G > 1 || sync)) return AMOE_EINVAL;
+  // G > 1: a rank that faults stores kAbortEpoch into every peer's done[] slot, and every rank
+  // checks those slots at each poll, so one rank's fault ends every rank's amoe_run with
+  // AMOE_EDEVICE instead of leaving the others polling for its done flag. AMOE_RUN_TIMEOUT
+  // (seconds, default 600; 0 = off) bounds a run whose legs were lost without a latched fault.
+  double timeout_s = 600.0;
+  if (const char* te = getenv("AMOE_RUN_TIMEOUT")) timeout_s = atof(te);
+  auto abort_run = [&](uint32_t code, uint32_t a0, uint32_t a1, uint32_t a2) -> amoe_status {
+    if (code) host_latch(c, code, a0, a1, a2, s);
+    if (c->cfg.G > 1) {
+      c->launches += launch_announce(c->dc, kAbortEpoch, 0, s);
+      cudaStreamSynchronize(s);
+    }
+    finish(stats);
+    return AMOE_EDEVICE;
+  };
   for (;;) {
     st = snapshot(c, s);   // waits for this rank's previous launches: the GPU is idle from here
     if (st != AMOE_OK) return st;
     const auto t_poll = clk::now();
     const char* snap = reinterpret_cast<const char*>(c->pinned);
-    if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return AMOE_EDEVICE;
+    if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return abort_run(0, 0, 0, 0);
+    if (c->cfg.G > 1) {
+      const uint32_t* dn = reinterpret_cast<const uint32_t*>(snap + c->lay.done);
+      for (int r = 0; r < c->cfg.G; ++r)
+        if (r != c->cfg.rank && dn[r] == kAbortEpoch) return abort_run(F_PEER_ABORT, (uint32_t)r, 0, 0);
+      const double el = std::chrono::duration<double>(t_poll - t_run0).count();
+      if (timeout_s > 0 && el > timeout_s) {
+        const uint64_t* sv0 = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
+        return abort_run(F_RUN_TIMEOUT, (uint32_t)el, (uint32_t)(sv0[0] - merged0), (uint32_t)expected);
+      }
+    }
     const uint64_t* sv = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
     log_executions(c, false);
     if (sync && !announced && !stepping) {
@@ -910,8 +948,22 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         break;
       }
       if (c->cfg.G == 1 && !announced && !sync_arrived) {
-        // single GPU: nothing queued and tokens not retired means a lost leg
+        // single GPU: nothing queued and tokens not retired means a lost leg. Name the first
+        // stranded token (admitted, not retired: SPEC.md L401's audit) in the error word:
+        // F_LOST_LEG (slot, layer, pieces of its legs that came back)
         rs.token_layers = (int64_t)(sv[0] - merged0);
+        const int T = c->cfg.T_slots;
+        std::vector<uint64_t> tt((size_t)2 * T);
+        std::vector<uint32_t> ld(T);
+        std::vector<int32_t> tl(T);
+        cudaMemcpy(tt.data(), c->ws + c->lay.tok_time, tt.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(ld.data(), c->ws + c->lay.legs_done, ld.size() * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(tl.data(), c->ws + c->lay.tok_layer, tl.size() * 4, cudaMemcpyDeviceToHost);
+        for (int t = 0; t < T; ++t)
+          if (tt[2 * t] != 0 && tt[2 * t + 1] == 0) {
+            host_latch(c, F_LOST_LEG, (uint32_t)t, (uint32_t)tl[t], ld[t], s);
+            break;
+          }
         finish(stats);
         return AMOE_EDEVICE;
       }

@@ -1459,14 +1459,19 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
 #ifdef AMOE_TRACE
   if (const char* g = getenv("AMOE_TRACE_GRID")) num_sms = std::min(num_sms, atoi(g));   // diagnostic
 #endif
-  static bool attr_done = false;
-  if (!attr_done) {
+  // the smem attribute is per device: contexts on several devices of one process (peer
+  // workspaces, amoe_import_peers) each need it set on their own device
+  static bool attr_done[64] = {false};
+  int dev_id = 0;
+  cudaGetDevice(&dev_id);
+  if (dev_id < 0 || dev_id >= 64) dev_id = 0;
+  if (!attr_done[dev_id]) {
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_GATEUP, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_DOWN, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(ffn_tc_kernel<MODE_DOWN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_GATEUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
     cudaFuncSetAttribute(tc2::ffn_tc2_kernel<MODE_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2_BYTES);
-    attr_done = true;
+    attr_done[dev_id] = true;
   }
   FfnArgs a{};
   a.nq = f.nq;

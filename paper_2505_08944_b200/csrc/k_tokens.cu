@@ -581,39 +581,38 @@ int launch_enqueue(const DevCtx& c, int layer, const int32_t* slots, int n, cons
 }
 
 template <typename T, int KSM, bool GATE>
-static void launch_combine_t(const DevCtx& c, int retire_pass, cudaStream_t s) {
+static void launch_combine_t(const DevCtx& c, int retire_pass, int num_sms, cudaStream_t s) {
   // persistent grid: every resident CTA slot once (no tail wave), capped by the worst case (all
-  // homed tokens ready); CTAs loop over 32-token chunks of the ready list
-  static int occ = 0, sms = 0;
+  // homed tokens ready); CTAs loop over 32-token chunks of the ready list. Occupancy is a
+  // property of the kernel (same on every B200); the SM count is the context's (AMOE_NUM_SMS
+  // partitions in the G-rank emulation)
+  static int occ = 0;
   if (!occ) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, combine_kernel<T, KSM, GATE>, kTokThreads, 0);
     if (occ < 1) occ = 1;
   }
   int grid = (c.T + kTPC - 1) / kTPC;
-  if (grid > sms * occ) grid = sms * occ;
+  if (grid > num_sms * occ) grid = num_sms * occ;
   launch_pdl(combine_kernel<T, KSM, GATE>, dim3(grid), dim3(kTokThreads), 0, s, c, retire_pass);
 }
 
 template <typename T, bool GATE>
-static void launch_combine_g(const DevCtx& c, int retire_pass, cudaStream_t s) {
+static void launch_combine_g(const DevCtx& c, int retire_pass, int num_sms, cudaStream_t s) {
   const int ksm = c.KS <= 2 ? 2 : c.KS <= 4 ? 4 : c.KS <= 8 ? 8 : 12;
-  if (ksm == 2) launch_combine_t<T, 2, GATE>(c, retire_pass, s);
-  else if (ksm == 4) launch_combine_t<T, 4, GATE>(c, retire_pass, s);
-  else if (ksm == 8) launch_combine_t<T, 8, GATE>(c, retire_pass, s);
-  else launch_combine_t<T, 12, GATE>(c, retire_pass, s);
+  if (ksm == 2) launch_combine_t<T, 2, GATE>(c, retire_pass, num_sms, s);
+  else if (ksm == 4) launch_combine_t<T, 4, GATE>(c, retire_pass, num_sms, s);
+  else if (ksm == 8) launch_combine_t<T, 8, GATE>(c, retire_pass, num_sms, s);
+  else launch_combine_t<T, 12, GATE>(c, retire_pass, num_sms, s);
 }
 
-int launch_combine(const DevCtx& c, int retire_pass, cudaStream_t s) {
+int launch_combine(const DevCtx& c, int retire_pass, int num_sms, cudaStream_t s) {
   launch_pdl(cdrain_kernel, dim3(1), dim3(32), 0, s, c);
   if (c.dtype == AMOE_BF16) {
-    if (c.gate_on) launch_combine_g<__nv_bfloat16, true>(c, retire_pass, s);
-    else launch_combine_g<__nv_bfloat16, false>(c, retire_pass, s);
+    if (c.gate_on) launch_combine_g<__nv_bfloat16, true>(c, retire_pass, num_sms, s);
+    else launch_combine_g<__nv_bfloat16, false>(c, retire_pass, num_sms, s);
   } else {
-    if (c.gate_on) launch_combine_g<float, true>(c, retire_pass, s);
-    else launch_combine_g<float, false>(c, retire_pass, s);
+    if (c.gate_on) launch_combine_g<float, true>(c, retire_pass, num_sms, s);
+    else launch_combine_g<float, false>(c, retire_pass, num_sms, s);
   }
   return 2;
 }

@@ -253,3 +253,54 @@ def test_gate_logits_brute_force_and_one_hot():
     # routing with a one-hot gate picks the largest coordinates of x among `cols`
     idx, _ = nx.route_topk(nx.gate_logits(x, onehot), 1)
     assert all(x[t, cols[idx[t, 0]]] == max(x[t, c] for c in cols) for t in range(5))
+
+
+# ---------------------------------------------------------------- SURVEY.md §8(c) FFN pins
+
+
+def _experts(g, E, d, ff):
+    return [tuple(nx.bf16_round(g.standard_normal(s) / np.sqrt(s[1])) for s in ((ff, d), (ff, d), (d, ff)))
+            for _ in range(E)]
+
+
+def test_k_equals_e_with_equal_logits_is_the_mean_of_the_experts():
+    """K = E with equal logits: every token visits every expert in index order (tie rule c12)
+    with weight exactly 1/E (softmax of equal values, E a power of two), so the layer adds the
+    plain mean of all experts' outputs — the closed form, evaluated in float64 here, must agree
+    within the storage rounding of h_new (one bf16 ulp) on every element. A dropped leg, a
+    wrong weight or a leg merged twice moves rows by ~1/E of an expert output."""
+    g = np.random.default_rng(21)
+    T, E, d, ff = 12, 4, 32, 48
+    h = nx.bf16_round(g.standard_normal((T, d)))
+    W = _experts(g, E, d, ff)
+    r = nx.moe_layer(h, np.zeros((T, E), np.float32), W, K=E)
+    assert np.array_equal(r["idx"], np.tile(np.arange(E), (T, 1)))
+    assert np.all(r["w"] == np.float32(1.0 / E))
+    x = nx.rmsnorm(h)
+    mean = np.mean([nx.expert_ffn(x, *w).astype(np.float64) for w in W], axis=0)
+    ref = h.astype(np.float64) + mean
+    ulp = 2.0 ** (np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+    assert np.all(np.abs(r["h_new"] - ref) <= ulp)
+    # a layer with one expert's leg dropped is far outside that bound
+    legs = r["legs"].copy()
+    legs[:, E - 1] = 0
+    bad = nx.combine(h, r["w"], legs)
+    assert np.max(np.abs(bad - ref) / ulp) > 4
+
+
+def test_point_mass_router_uses_only_expert_zero():
+    """A router whose logits put all mass on expert 0 (others -inf) with K = 1: every token's
+    single leg goes to expert 0 with weight 1, so the layer is h + SwiGLU_0(rmsnorm(h)) and the
+    other experts' weights are never read (replacing them with NaN changes nothing)."""
+    g = np.random.default_rng(22)
+    T, E, d, ff = 9, 8, 32, 64
+    h = nx.bf16_round(g.standard_normal((T, d)))
+    W = _experts(g, E, d, ff)
+    z = np.full((T, E), -np.inf, np.float32)
+    z[:, 0] = 0.0
+    r = nx.moe_layer(h, z, W, K=1)
+    assert np.all(r["idx"] == 0) and np.all(r["w"] == 1.0)
+    x = nx.rmsnorm(h)
+    assert np.array_equal(r["h_new"], nx.bf16_round(h + nx.expert_ffn(x, *W[0])))
+    Wn = [W[0]] + [tuple(np.full_like(a, np.nan) for a in w) for w in W[1:]]
+    assert np.array_equal(nx.moe_layer(h, z, Wn, K=1)["h_new"], r["h_new"])
