@@ -193,6 +193,17 @@ amoe_status amoe_set_router(amoe_ctx_t ctx, const float* table, int n_tables);
  * 4096 (bf16) / 2048 (fp32). Synchronous (16-byte H2D copy). */
 amoe_status amoe_set_gate(amoe_ctx_t ctx, int layer, const void* wg, const float* bias);
 
+/* Checked mode (schedule replay): every drain (amoe_rebatch and the
+ * drains inside amoe_run's launches) appends, per nonempty queue it drained, an execution record
+ * and a copy of the legs it took, in FIFO order, to `buf` (device, caller-owned, 16-B aligned;
+ * NULL turns logging off). Layout, uint32 words: [0] executions logged, [1] legs logged,
+ * [2] record capacity, [3] leg capacity (both set here from `bytes`), [4..8) reserved; then
+ * records {qid = layer * H + local queue, start = ring position of the first drained leg, n,
+ * offset of its first leg} x capacity; then amoe_leg x capacity, with `seq` replaced by the
+ * token's pass. Counts beyond capacity are counted, not written. Slows drains (one CTA copies
+ * the legs): tests only. Synchronises the device. */
+amoe_status amoe_set_exec_log(amoe_ctx_t ctx, void* buf, size_t bytes);
+
 /* Admit tokens: for i < T, slot = slots[i] (device int32): h[slot] = h0[i] (device [T, d]
  * storage dtype), x[slot] = rmsnorm(h0[i]), pass = pass, layer = 0, pool cleared. */
 amoe_status amoe_token_init(amoe_ctx_t ctx, const int32_t* slots, int T, const void* h0, int pass,

@@ -127,6 +127,42 @@ class Box:
         self.trace_drain.append((rank, layer, expert, legs))
         return legs
 
+    def drain_given(self, rank: int, layer: int, expert: int, keys) -> list[Leg]:
+        """Replay one drain another executor performed (any pick
+        sequence is a legal schedule). PAPER.md L222: "executor drains the selected queue" — the
+        legs it took, keys = [(token, k, pass)], must all be queued in µ-queue (rank, layer,
+        expert); they are removed and marked drained. A leg that is not queued there (never routed
+        to this expert, drained before, or duplicated within the drain) is a conservation
+        violation. Which queued legs an executor may take is timing (what had arrived), so the
+        replay checks membership, not the oracle's FIFO position; FIFO contiguity is a property
+        of the executor's own ring, checked by the caller."""
+        q = self.queues.get((rank, layer, expert))
+        if q is None:
+            raise ConservationError(f"queue (rank {rank}, layer {layer}, expert {expert}) is not hosted there")
+        want = {}
+        for key in keys:
+            key = (int(key[0]), int(key[1]), int(key[2]))
+            if key in want:
+                raise ConservationError(f"leg {key} appears twice in one drain")
+            want[key] = True
+        kept, taken = deque(), []
+        for leg in q.q:
+            key = (leg.token, leg.k, leg.pass_idx)
+            if want.pop(key, None):
+                taken.append(leg)
+            else:
+                kept.append(leg)
+        if want:
+            t, k, p = next(iter(want))
+            seen = (t, layer, p, k) in self.seen
+            raise ConservationError(f"leg (token {t}, k {k}, pass {p}) drained from (layer {layer}, expert {expert}) "
+                                    + ("twice" if seen else "but never queued there"))
+        q.q = kept
+        for g in taken:
+            self.seen.add((g.token, g.layer, g.pass_idx, g.k))
+        self.trace_drain.append((rank, layer, expert, taken))
+        return taken
+
     def audit_quiescent(self):
         """At quiescence: every enqueued leg drained exactly once; pool empty."""
         enq = {(t, l, p, k) for (t, l, p, k, _) in self.trace_enq}

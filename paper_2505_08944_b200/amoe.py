@@ -65,6 +65,7 @@ EXPORTS = {
     "amoe_import_peers": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]),
     "amoe_set_expert": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "amoe_set_router": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "amoe_set_exec_log": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
     "amoe_set_gate": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "amoe_token_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     "amoe_enqueue": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -285,6 +286,35 @@ class Context:
         self._gates = getattr(self, "_gates", {})
         self._gates[layer] = (wg, bias)         # borrowed by the library: keep alive
         self._chk(self.lib.amoe_set_gate(self.h, layer, _p(wg), _p(bias)), "amoe_set_gate")
+
+    def set_exec_log(self, nbytes: int | None = 1 << 24):
+        """Checked mode: log every drain's legs into a device buffer of nbytes (None = off)."""
+        if nbytes is None:
+            self._xlog = None
+            self._chk(self.lib.amoe_set_exec_log(self.h, None, 0), "amoe_set_exec_log")
+            return
+        self._xlog = torch.zeros(nbytes // 16 * 16, dtype=torch.uint8, device=self.device)
+        self._chk(self.lib.amoe_set_exec_log(self.h, _p(self._xlog), self._xlog.numel()), "amoe_set_exec_log")
+
+    def read_exec_log(self):
+        """[(layer, local queue, start, [(slot, k, home, w, pass), ...]), ...] in drain order.
+        Raises if the buffer overflowed."""
+        import numpy as np
+        b = self._xlog.cpu().numpy()
+        w = b.view(np.uint32)
+        ne, nl, cap_e, cap_l = (int(v) for v in w[:4])
+        if ne > cap_e or nl > cap_l:
+            raise RuntimeError(f"exec log overflow: {ne}/{cap_e} records, {nl}/{cap_l} legs")
+        rec = w[8:8 + 4 * ne].reshape(ne, 4)
+        legs = b[(8 + 4 * cap_e) * 4:].view(np.int32).reshape(-1, 4)[:nl]
+        out = []
+        for qid, start, n, off in rec.tolist():
+            lg = legs[off:off + n]
+            kh = lg[:, 1].view(np.uint32)
+            out.append((qid // self.H, qid % self.H, start,
+                        list(zip(lg[:, 0].tolist(), (kh & 0xFFFF).tolist(), (kh >> 16).tolist(),
+                                 lg[:, 2].view(np.float32).tolist(), lg[:, 3].tolist()))))
+        return out
 
     def local_queue(self, expert):
         return self.lib.amoe_local_queue(self.h, expert)

@@ -74,6 +74,7 @@ struct DevCtx {
   int32_t n_tab;
   const float* router;               // local [n_tab][L][T][E] or null
   int32_t gate_on;                   // some layer has a router gate (amoe_set_gate)
+  uint32_t* xlog;                    // checked-mode execution log (amoe_set_exec_log) or null
   int32_t die_cnt[2];                // SMs on each die (die_probe); die_cnt[1] == 0: no die split
   int32_t pad_die;
   uint64_t die_mask[4];              // bit smid set: SM on die 1
@@ -162,6 +163,15 @@ __device__ __forceinline__ void raise_fault(const DevCtx& c, uint32_t code, uint
     e[1] = a0; e[2] = a1; e[3] = a2;
     __threadfence();
   }
+}
+
+// ------------------------------------------------------------------ checked-mode execution log
+// (amoe_set_exec_log): header u32[8] {executions, legs, exec capacity, leg capacity}, then exec
+// records u32[4] {qid, start, n, leg offset}, then the drained legs (amoe_leg, seq := pass).
+constexpr int kXlogHeader = 8;
+__device__ __forceinline__ uint32_t* xlog_exec(uint32_t* xl) { return xl + kXlogHeader; }
+__device__ __forceinline__ amoe_leg* xlog_legs(uint32_t* xl) {
+  return reinterpret_cast<amoe_leg*>(xl + kXlogHeader + 4 * (uint64_t)xl[2]);
 }
 
 // ------------------------------------------------------------------ µ-queue rings

@@ -379,6 +379,23 @@ amoe_status amoe_set_gate(amoe_ctx_t c, int layer, const void* wg, const float* 
   return AMOE_OK;
 }
 
+amoe_status amoe_set_exec_log(amoe_ctx_t c, void* buf, size_t bytes) {
+  if (!c) return AMOE_EINVAL;
+  if (!buf) { c->dc.xlog = nullptr; return AMOE_OK; }
+  if ((reinterpret_cast<uintptr_t>(buf) & 15) || bytes < (kXlogHeader + 4) * 4 + 16) return AMOE_EINVAL;
+  // split the buffer: one 16-B exec record per 16 drained legs (an execution drains >= 1 leg)
+  const uint64_t body = bytes - kXlogHeader * 4;
+  uint64_t cap_e = body / 16 / 8;
+  if (cap_e < 1) cap_e = 1;
+  const uint64_t cap_l = (body - cap_e * 16) / 16;
+  if (cap_l < 1 || cap_e > 0xffffffffu || cap_l > 0xffffffffu) return AMOE_EINVAL;
+  const uint32_t hdr[kXlogHeader] = {0, 0, (uint32_t)cap_e, (uint32_t)cap_l, 0, 0, 0, 0};
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(buf, hdr, sizeof(hdr), cudaMemcpyHostToDevice));
+  c->dc.xlog = static_cast<uint32_t*>(buf);
+  return AMOE_OK;
+}
+
 amoe_status amoe_set_router(amoe_ctx_t c, const float* table, int n_tables) {
   if (!c || !table || n_tables < 1) return AMOE_EINVAL;
   c->dc.router = table;

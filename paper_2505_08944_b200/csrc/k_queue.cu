@@ -25,6 +25,47 @@ bool pdl_enabled() {
 
 constexpr int kDrainThreads = 128;
 
+// Checked mode: append one record per nonempty drained queue and a copy of its drained legs
+// (seq replaced by the token's pass, read from its home's token state) to the execution log.
+// Called by every thread of the draining CTA after avail[]/head[] are final.
+__device__ void xlog_drain(const DevCtx& c, int nq, const int32_t* qid, const uint32_t* head, const uint32_t* avail) {
+  __shared__ uint32_t s_e0, s_l0;
+  __shared__ uint32_t s_off[AMOE_MAX_GROUP];
+  uint32_t* xl = c.xlog;
+  if (threadIdx.x == 0) {
+    uint32_t ne = 0, nl = 0;
+    for (int q = 0; q < nq; ++q)
+      if (avail[q]) { s_off[q] = nl; nl += avail[q]; ++ne; }
+    s_e0 = atomicAdd(xl + 0, ne);
+    s_l0 = atomicAdd(xl + 1, nl);
+    uint32_t e = s_e0;
+    for (int q = 0; q < nq; ++q)
+      if (avail[q]) {
+        if (e < xl[2]) {
+          uint32_t* r = xlog_exec(xl) + 4 * (uint64_t)e;
+          r[0] = (uint32_t)qid[q]; r[1] = head[q]; r[2] = avail[q]; r[3] = s_l0 + s_off[q];
+        }
+        ++e;
+      }
+  }
+  __syncthreads();
+  amoe_leg* legs = xlog_legs(xl);
+  const uint32_t cap = xl[3];
+  for (int q = 0; q < nq; ++q) {
+    if (!avail[q]) continue;
+    const amoe_leg* ring = ring_ptr(c, c.rank, qid[q]);
+    for (uint32_t i = threadIdx.x; i < avail[q]; i += blockDim.x) {
+      const uint32_t o = s_l0 + s_off[q] + i;
+      if (o >= cap) break;
+      amoe_leg e = ring[(head[q] + i) & c.ring_mask];
+      const int home = (e.home >= 0 && e.home < c.G) ? e.home : c.rank;
+      const int slot = (e.token_slot >= 0 && e.token_slot < c.T) ? e.token_slot : 0;
+      e.seq = (uint32_t)reinterpret_cast<const int32_t*>(c.peer[home] + c.lay.tok_pass)[slot];
+      legs[o] = e;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kDrainThreads) drain_kernel(DevCtx c, GroupDev g) {
   AMOE_PDL_ENTRY();
   __shared__ uint32_t avail[AMOE_MAX_GROUP], head[AMOE_MAX_GROUP], rv[AMOE_MAX_GROUP];
@@ -86,6 +127,7 @@ __global__ void __launch_bounds__(kDrainThreads) drain_kernel(DevCtx c, GroupDev
   }
   __syncthreads();
   for (int q = tid; q < g.nq; q += blockDim.x) qctr_ptr(c, c.rank, g.qid[q])[2] = head[q] + avail[q];
+  if (c.xlog) xlog_drain(c, g.nq, g.qid, head, avail);
 }
 
 // Locate the queue of row-rank r in a group (prefix sums of n in shared memory).

@@ -95,3 +95,46 @@ class Problem:
                     ctx.set_expert(l, e, *self.Wd[(l, e)])
         ctx.set_router(torch.from_numpy(self.tables[rank]).cuda().contiguous())
         return ctx
+
+
+def replay_exec_log(L, E, K, S, G, T, logits_fn, n_passes, logs, q2e, fresh=True):
+    """Schedule replay. logs[r] = rank r's drains in order, each
+    (layer, local queue, ring start, [(slot, k, home, w, pass), ...]) as Context.read_exec_log
+    returns them; q2e[r] maps rank r's local queue index to the expert id (E + j = shared j).
+    The oracle's µ-queue model (oracle.queues.Box over G ranks) is filled with every routed leg
+    of passes 0..n_passes-1 (routing is a pure function of the synthetic logits), then every
+    logged drain is replayed through Box.drain_given, which checks bit-exactly that each drained
+    leg was queued at that (rank, layer, expert) for that pass and is taken once. Also checked:
+    consecutive drains of a ring are contiguous (each takes the oldest entries after the last
+    one, from position 0 on a fresh context), each leg's weight is the router's (|Δw| <= 1e-6),
+    and at the end every leg was drained exactly once (Box.audit_quiescent names a lost one).
+    Returns the Box and the per-(rank, layer, expert, pass) drained counts."""
+    from oracle.queues import Box
+    box = Box(L=L, E=E, K=K, S=S, G=G, T=T)
+    wref = {}
+    for p in range(n_passes):
+        for l in range(L):
+            idx, w = nx.route_topk(logits_fn(p, l), K)
+            box.enqueue(l, p, range(G * T), idx, w)
+            for t in range(G * T):
+                for k in range(K):
+                    wref[(t, k, p, l)] = float(w[t, k])
+    counts = {}
+    for r, log in enumerate(logs):
+        nxt = {}
+        for (l, q, start, legs) in log:
+            e = q2e[r][q]
+            if (l, q) in nxt:
+                assert start == nxt[(l, q)], f"rank {r} ring ({l},{q}): drain at {start}, expected {nxt[(l, q)]}"
+            elif fresh:
+                assert start == 0, f"rank {r} ring ({l},{q}): first drain at {start}"
+            nxt[(l, q)] = start + len(legs)
+            keys = [(home * T + slot, k, ps) for slot, k, home, _, ps in legs]
+            box.drain_given(r, l, e, keys)
+            for (slot, k, home, wv, ps) in legs:
+                ref = wref[(home * T + slot, k, ps, l)] if k < K else 1.0
+                assert abs(wv - ref) <= 1e-6, (r, l, e, slot, k, wv, ref)
+                key = (r, l, e, ps)
+                counts[key] = counts.get(key, 0) + 1
+    box.audit_quiescent()
+    return box, counts

@@ -43,6 +43,7 @@ def _rank_main(rank, world, port, T, q):
             for e in D.hosted_experts(P.E, P.S, world, rank):
                 ctx.set_expert(l, e, *P.Wd[(l, e)])
         ctx.set_router(torch.from_numpy(P.tables[rank]).cuda().contiguous())
+        ctx.set_exec_log(1 << 22)
         torch.cuda.synchronize()
         dist.barrier()           # all workspaces created (zeroed) before any rank pushes legs
         slots = torch.arange(T, dtype=torch.int32, device="cuda")
@@ -52,12 +53,13 @@ def _rank_main(rank, world, port, T, q):
         stats = ctx.run(retire_pass=2)
         torch.cuda.synchronize()
         ctx.check()
-        q.put((rank, to_np(ctx.state()["h"]), stats, int(ctx.state()["stats"][3])))
+        q2e = {ctx.local_queue(e): e for e in D.hosted_experts(P.E, P.S, world, rank)}
+        q.put((rank, to_np(ctx.state()["h"]), stats, int(ctx.state()["stats"][3]), ctx.read_exec_log(), q2e))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - surfaced by the parent
         import traceback
-        q.put((rank, None, traceback.format_exc(), 0))
+        q.put((rank, None, traceback.format_exc(), 0, None, None))
 
 
 def test_two_processes_one_gpu_match_single_rank():
@@ -72,9 +74,9 @@ def test_two_processes_one_gpu_match_single_rank():
         p.start()
     res = {}
     for _ in range(world):
-        r, h, stats, remote = q.get(timeout=300)
+        r, h, stats, remote, log, q2e = q.get(timeout=300)
         assert h is not None, stats
-        res[r] = (h, stats, remote)
+        res[r] = (h, stats, remote, log, q2e)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -92,4 +94,17 @@ def test_two_processes_one_gpu_match_single_rank():
     c1.run(retire_pass=2)
     torch.cuda.synchronize()
     h1 = to_np(c1.state()["h"])
-    assert np.array_equal(np.concatenate([res[0][0], res[1][0]]), h1)
+    h = np.concatenate([res[0][0], res[1][0]])
+    assert np.array_equal(h, h1)
+    # against the oracle: every drain of both processes replayed through Box(G=2), per-rank leg
+    # counts = the legs routed to its experts, h vs the synchronous run (reading c13)
+    from oracle import drivers
+    from parity_util import TOL, floored_err, host_values, replay_exec_log
+    _, counts = replay_exec_log(P.L, P.E, P.K, P.S, world, T, P.logits, 2, [res[r][3] for r in range(world)],
+                                [res[r][4] for r in range(world)])
+    for r in range(world):
+        assert res[r][1]["legs"] == sum(v for k, v in counts.items() if k[0] == r)
+    W, SH = P.oracle_weights()
+    ref, _ = drivers.sync_run(np.concatenate([host_values(x, "bf16") for x in P.h0]), P.logits, W, P.K,
+                              n_passes=2, shared=SH)
+    assert floored_err(h, ref) <= TOL["bf16"]

@@ -206,3 +206,58 @@ def test_async_equals_sync_over_every_schedule(T, E, caps, expect):
         assert np.array_equal(h, ref)
         n += 1
     assert n == expect, n          # schedules enumerated for this seeded routing
+
+
+def _trace_as_log(box, G):
+    """The oracle async driver's own drain trace in Context.read_exec_log's format (local queue
+    index := expert id, ring positions contiguous per queue)."""
+    logs = [[] for _ in range(G)]
+    pos = {}
+    for (r, l, e, legs) in box.trace_drain:
+        start = pos.get((r, l, e), 0)
+        pos[(r, l, e)] = start + len(legs)
+        logs[r].append((l, e, start, [(g.token % box.T, g.k, g.home, g.w, g.pass_idx) for g in legs]))
+    return logs
+
+
+def test_replay_accepts_a_legal_schedule_and_rejects_tampering():
+    """The schedule-replay checker the GPU tests use (tests/parity_util.replay_exec_log, built on
+    oracle.queues.Box.drain_given), pinned on the oracle's own randomised schedules: a legal
+    drain sequence replays; a leg drained twice, a leg taken from the wrong expert's queue, a
+    lost leg and a gap in a ring each fail with the token named."""
+    from parity_util import replay_exec_log
+    G, T, L, E, K = 2, 4, 2, 4, 2
+    h0, logits, W, _ = _tiny_problem(5, N=G * T, L=L, E=E)
+    _, box, _ = drivers.async_run(h0, logits, W, K=K, G=G, T=T, n_passes=2, seed=3, max_cap=2)
+    logs = _trace_as_log(box, G)
+    q2e = [{e: e for e in range(E)} for _ in range(G)]
+    _, counts = replay_exec_log(L, E, K, 0, G, T, logits, 2, logs, q2e)
+    for p in range(2):
+        for l in range(L):
+            idx, _ = nx.route_topk(logits(p, l), K)
+            hist = np.bincount(idx.ravel(), minlength=E)
+            for e in range(E):
+                assert counts.get((e % G, l, e, p), 0) == hist[e]
+    import copy
+    dup = copy.deepcopy(logs)
+    dup[0].append((dup[0][0][0], dup[0][0][1], 10 ** 6, dup[0][0][3][:1]))
+    with pytest.raises((ConservationError, AssertionError)):
+        replay_exec_log(L, E, K, 0, G, T, logits, 2, dup, q2e, fresh=False)
+    wrong = copy.deepcopy(logs)
+    l0, e0, s0, legs0 = wrong[0][0]
+    wrong[0][0] = (l0, (e0 + 2) % E, s0, legs0)          # same rank, another expert's queue
+    with pytest.raises((ConservationError, AssertionError)):
+        replay_exec_log(L, E, K, 0, G, T, logits, 2, wrong, q2e, fresh=False)
+    lost = copy.deepcopy(logs)
+    l0, e0, s0, legs0 = lost[1][-1]
+    lost[1][-1] = (l0, e0, s0, legs0[1:]) if len(legs0) > 1 else lost[1][-1]
+    if len(legs0) > 1:
+        with pytest.raises(ConservationError, match=f"token {legs0[0][2] * T + legs0[0][0]}"):
+            replay_exec_log(L, E, K, 0, G, T, logits, 2, lost, q2e, fresh=False)
+    gap = copy.deepcopy(logs)
+    for i, (l, e, s, legs) in enumerate(gap[0]):
+        if s > 0:
+            gap[0][i] = (l, e, s + 1, legs)
+            break
+    with pytest.raises(AssertionError, match="expected"):
+        replay_exec_log(L, E, K, 0, G, T, logits, 2, gap, q2e)
