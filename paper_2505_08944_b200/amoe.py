@@ -382,7 +382,7 @@ class Context:
                                           C.byref(p), C.byref(st), _stream(stream)), "amoe_pass_host")
         return st.as_dict()
 
-    STAGES = ("rebatch", "ffn_gateup", "ffn_down", "forward", "combine", "admit")
+    STAGES = ("rebatch", "ffn_gateup", "ffn_down", "forward", "combine", "admit", "ffn_cold")
 
     def profile_enable(self, on=True):
         self._chk(self.lib.amoe_profile_enable(self.h, 1 if on else 0), "amoe_profile_enable")

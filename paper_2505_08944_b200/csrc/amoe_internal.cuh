@@ -16,6 +16,7 @@ constexpr int kMaxKS = 12;          // K + S legs per token
 constexpr int kRowAlign = 128;      // group rows are allocated per queue in multiples of this
 constexpr int kSplitSlots = 512;    // split-K tile slots (counters)
 constexpr int kSplitUnits = 2048;   // split-K partial tiles (128 x 256 fp32 each): 256 MB
+constexpr int kColdCtr = 16384;     // cold-kernel flags and counters (u32), DESIGN.md §5.4
 
 // Device fault codes latched into the error word.
 enum Fault : uint32_t {
@@ -30,7 +31,7 @@ enum Fault : uint32_t {
   F_NO_ROUTER = 8,        // args: slot, layer, pass (needs amoe_set_router or amoe_set_gate)
   F_PEER_ABORT = 9,       // args: peer rank whose fault (or timeout) aborted this rank's amoe_run (host-latched)
   F_RUN_TIMEOUT = 10,     // args: seconds, merged, expected (host-latched: AMOE_RUN_TIMEOUT expired, G > 1)
-  F_LOST_LEG = 11,        // args: stranded token slot, its layer, leg pieces returned (host-latched, G == 1)
+  F_LOST_LEG = 11,        // args: stranded token slot, its layer, leg columns returned (host-latched, G == 1)
 };
 // done[] value a faulting rank stores into every peer: never equal to a run epoch
 constexpr uint32_t kAbortEpoch = 0xFFFFFFFFu;
@@ -48,6 +49,7 @@ struct Layout {
   uint64_t cinfo;      // i32[4]: combine drain n, start
   uint64_t sched;      // u32[4]: FFN die-aware tile claims {die 0, die 1, finished clusters, pad}
   uint64_t split_cnt;  // u32[kSplitSlots]: split-K arrival counters (self-resetting)
+  uint64_t cold;       // u32[kColdCtr]: cold fused kernel: drain flag, gather arrivals, exits, partial flags, act counts
   uint64_t h, x;       // [T][d]
   uint64_t pool;       // [T][K+S][d]
   uint64_t legs_done;  // u32[T]
@@ -196,11 +198,12 @@ __device__ __forceinline__ void write_leg(amoe_leg* ring, uint32_t mask, uint32_
 }
 
 // ------------------------------------------------------------------ token pool (a7 -> a8)
-// A leg's output row is returned in pieces of 128 columns (the fused down-GEMM epilogue stores
-// one N tile at a time); the token is complete when all (K+S) * d/128 pieces arrived.
-__device__ __forceinline__ uint32_t pieces_per_token(const DevCtx& c) { return (uint32_t)c.KS * (uint32_t)(c.d / 128); }
+// A leg's output row is returned in pieces (column ranges: the fused down-GEMM epilogues store
+// one N tile, or one slice of a split tile, at a time), counted in columns; the token is
+// complete when all (K+S) * d columns of its legs arrived.
+__device__ __forceinline__ uint32_t pieces_per_token(const DevCtx& c) { return (uint32_t)c.KS * (uint32_t)c.d; }
 
-// Count `pieces` returned pieces of token `slot` on `home` (release: the caller's pool stores
+// Count `pieces` returned columns of token `slot` on `home` (release: the caller's pool stores
 // happen before); the arrival completing the token appends it to the home's combine ring.
 __device__ __forceinline__ void leg_pieces_done(const DevCtx& c, int home, int slot, int k, uint32_t pieces) {
   const bool sys = c.G > 1;

@@ -24,6 +24,8 @@ int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                   const CUtensorMap&, void*, void*, const amoe_leg*, int, int, int, cudaStream_t, int);
+int launch_ffn_cold(const DevCtx&, int, const int*, const int*, int, const CUtensorMap&, const CUtensorMap&, void*, void*,
+                    int32_t*, const CUtensorMap*, uint32_t, int, cudaStream_t);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
 int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
 }  // namespace amoe
@@ -71,9 +73,10 @@ struct amoe_ctx {
   // executions logged by amoe_run while profiling: (l*H + q, drained legs), from the ring heads
   std::vector<uint32_t> prev_head;
   std::vector<int32_t> exec_log;
+  uint32_t cold_seq = 0;              // launches of the fused cold kernel (tags its partial flags)
 };
 
-enum Stage { ST_REBATCH = 0, ST_GATEUP = 1, ST_DOWN = 2, ST_FORWARD = 3, ST_COMBINE = 4, ST_ENQUEUE = 5 };
+enum Stage { ST_REBATCH = 0, ST_GATEUP = 1, ST_DOWN = 2, ST_FORWARD = 3, ST_COMBINE = 4, ST_ENQUEUE = 5, ST_COLD = 6 };
 
 static cudaEvent_t ev_get(amoe_ctx* c) {
   if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
@@ -185,6 +188,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->cinfo = take(16);
   L->sched = take(16);
   L->split_cnt = take((uint64_t)kSplitSlots * 4);
+  L->cold = take((uint64_t)kColdCtr * 4);
   L->h = take(T * d * es);
   L->x = take(T * d * es);
   L->pool = take(T * KS * d * es);
@@ -589,9 +593,64 @@ amoe_status amoe_expert_ffn_forward(amoe_ctx_t c, const amoe_group* g, void* str
   return expert_ffn(c, g, 1, (cudaStream_t)stream);
 }
 
+// The fused cold path (AMOE_COLD=1) vs the four-kernel path (default while the fused kernel is
+// being tuned: profiles/r02_cold_sweep.md).
+static bool cold_enabled() {
+  const char* e = getenv("AMOE_COLD");
+  return e && e[0] == '1';
+}
+
+// a4 + a5 + a6 + a7 in ONE launch for a cold pick (k_ffn_cold.cu): drain at most
+// caps[q] legs of each queue, gather, SwiGLU expert, store into the home pools. bf16 only;
+// every cap <= 128; the group's tile / act buffers hold nq * n_pad rows.
+static amoe_status cold_ffn_forward(amoe_ctx* c, const amoe_group* g, const int* caps, cudaStream_t s) {
+  GroupDev gd;
+  int wslot[AMOE_MAX_GROUP];
+  amoe_status st = make_group(c, g, 0, &gd, wslot);
+  if (st != AMOE_OK) return st;
+  if (c->cfg.dtype != AMOE_BF16 || !g->act) return AMOE_EINVAL;
+  int nmax = 1;
+  for (int q = 0; q < g->nq; ++q) {
+    if (caps[q] < 0 || caps[q] > 128) return AMOE_EINVAL;
+    nmax = std::max(nmax, caps[q]);
+    if (!c->hosted_flags[wslot[q] / 3]) return AMOE_EINVAL;
+  }
+  const int n_pad = (nmax + 15) / 16 * 16;
+  if ((int64_t)g->nq * n_pad > g->rows_cap) return AMOE_EINVAL;
+  for (int r = 0; r < c->cfg.G; ++r)
+    if (!c->dc.peer[r]) return AMOE_EPEER;
+  const CUtensorMap* p;
+  CUtensorMap mx, ma;
+  if (!(p = cached_map(c, g->tile, g->rows_cap, c->cfg.d, n_pad))) return AMOE_ECUDA;
+  mx = *p;
+  if (!(p = cached_map(c, g->act, g->rows_cap, c->cfg.ff, n_pad))) return AMOE_ECUDA;
+  ma = *p;
+  int qid[AMOE_MAX_GROUP];
+  for (int q = 0; q < g->nq; ++q) qid[q] = wslot[q] / 3;
+  {
+    StageTimer tm(c, ST_COLD, s);
+    c->launches += launch_ffn_cold(c->dc, g->nq, qid, caps, n_pad, mx, ma, g->tile, g->act, g->qinfo,
+                                   reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps), ++c->cold_seq,
+                                   c->num_sms, s);
+  }
+  c->last_stream = s;
+  CK(cudaGetLastError());
+  return AMOE_OK;
+}
+
 amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_tokens, void* stream) {
   if (!c) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  if (g && g->nq >= 1 && g->nq <= AMOE_MAX_GROUP && g->max_rows_hint >= 1 && g->max_rows_hint <= 128 &&
+      c->cfg.dtype == AMOE_BF16 && cold_enabled()) {
+    // cold pick: every queue drains at most the hint (and max_tokens / cfg.max_batch)
+    int cap = g->max_rows_hint;
+    if (max_tokens > 0) cap = std::min(cap, max_tokens);
+    if (c->cfg.max_batch > 0) cap = std::min(cap, c->cfg.max_batch);
+    int caps[AMOE_MAX_GROUP];
+    for (int q = 0; q < g->nq; ++q) caps[q] = cap;
+    return cold_ffn_forward(c, g, caps, s);
+  }
   // The fused gather is correct (tests) but slower on B200: each A row is re-read by every N tile
   // of its raster group and TMA tile::gather4 moves ~6.6 B/cycle/SM vs >40 for tiled loads
   // (profiles/r01_fused_gather.md), so the materialised gather (2·d bytes per leg, once) wins.
@@ -929,6 +988,15 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       // the second drain is stream-ordered behind the first group's forward.
       int n_cold = 0;
       for (int j = 0; j < g.nq; ++j) n_cold += group_rows(c, g, j, Q.data(), H) <= 128;
+      // cold pick: every queue drains <= 128 legs (its snapshot depth, or the max_batch cap)
+      int cold_caps[AMOE_MAX_GROUP];
+      bool cold_pick = c->cfg.dtype == AMOE_BF16 && cold_enabled();
+      for (int j = 0; j < g.nq && cold_pick; ++j) {
+        int cap = group_rows(c, g, j, Q.data(), H);
+        if (c->cfg.max_batch > 0) cap = std::min(cap, c->cfg.max_batch);
+        cold_caps[j] = cap;
+        cold_pick = cap <= 128;
+      }
       if (split_pick && n_cold > 0 && n_cold < g.nq) {
         amoe_group gc = g, gh = g;
         gc.nq = gh.nq = 0;
@@ -944,6 +1012,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         if ((st = amoe_rebatch_ffn_forward(c, &gc, 0, s)) != AMOE_OK) return st;
         if ((st = amoe_rebatch_ffn_forward(c, &gh, 0, s)) != AMOE_OK) return st;
         rs.picks += 1;   // one pick, two launches
+      } else if (cold_pick) {
+        // every queue of the pick is cold: the fused one-launch path, each queue drained up to
+        // the depth this pick saw (its published prefix at the snapshot)
+        if ((st = cold_ffn_forward(c, &g, cold_caps, s)) != AMOE_OK) return st;
+        rs.picks += 1;
       } else {
         if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;
         rs.picks += 1;
@@ -967,7 +1040,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       if (c->cfg.G == 1 && !announced && !sync_arrived) {
         // single GPU: nothing queued and tokens not retired means a lost leg. Name the first
         // stranded token (admitted, not retired: SPEC.md L401's audit) in the error word:
-        // F_LOST_LEG (slot, layer, pieces of its legs that came back)
+        // F_LOST_LEG (slot, layer, columns of its legs that came back)
         rs.token_layers = (int64_t)(sv[0] - merged0);
         const int T = c->cfg.T_slots;
         std::vector<uint64_t> tt((size_t)2 * T);

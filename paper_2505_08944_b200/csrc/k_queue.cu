@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(kRowThreads) forward_kernel(DevCtx c, GroupDev
       fence_sc(sys);       // the whole warp's row stores before the counter (cumulativity)
       atomicAdd(&s_legs, 1ull);
       if (home != c.rank) atomicAdd(&s_remote, 1ull);
-      // the whole row = d/128 pieces; the completing arrival appends to the combine ring
-      leg_pieces_done(c, home, e.token_slot, e.k, (uint32_t)(c.d / 128));
+      // the whole row = d columns; the completing arrival appends to the combine ring
+      leg_pieces_done(c, home, e.token_slot, e.k, (uint32_t)c.d);
     }
   }
   __syncthreads();

@@ -218,8 +218,8 @@ def test_layer_fullsize_every_m_tile(shape):
     - Numerics, every M tile: from every execution, one random row out of every 128-row block
       of its drained legs (each CTA's half of every 256-row pair tile, ragged tails included),
       plus its last row, is recomputed by the float64 oracle from the GPU's own x and compared,
-      all columns, with the row the fused epilogue stored into the home token pool (floored 2e-2,
-      max row-L2 <= 2e-3).
+      all columns, with the row the fused epilogue stored into the home token pool (floored 2e-2;
+      row-L2 mean <= 1e-3 and max <= 4e-3, reading c13).
     - The merge of every token is bit-exact (teacher-forced on the GPU's pool and weights) and
       x_{l+1} is within one bf16 ulp of rmsnorm(h)."""
     from parity_util import replay_exec_log, ulp_err
@@ -262,7 +262,7 @@ def test_layer_fullsize_every_m_tile(shape):
         got = pool[sl, ks]
         assert floored_err(got, ref) <= TOL["bf16"], (e, floored_err(got, ref))
         rl2 = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
-        assert rl2.max() <= 2e-3, (e, rl2.max())
+        assert rl2.mean() <= 1e-3 and rl2.max() <= 4e-3, (e, rl2.mean(), rl2.max())   # reading c13
         checked += len(rows)
     assert checked >= sum(-(-len(x[3]) // 128) for x in log)
     w_gpu = st["tok_w"].cpu().numpy()

@@ -29,7 +29,9 @@ def _rank_main(rank, world, port, T, q):
         sys.path.insert(0, root)
         sys.path.insert(0, os.path.join(root, "tests"))
         import torch.distributed as dist
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        # bitwise vs one rank: unsplit FFN path only (the cold kernel's split order depends on
+        # the pick's shape)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), AMOE_COLD="0")
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         from paper_2505_08944_b200 import amoe, dist as D
@@ -62,7 +64,8 @@ def _rank_main(rank, world, port, T, q):
         q.put((rank, None, traceback.format_exc(), 0, None, None))
 
 
-def test_two_processes_one_gpu_match_single_rank():
+def test_two_processes_one_gpu_match_single_rank(monkeypatch):
+    monkeypatch.setenv("AMOE_COLD", "0")
     if not torch.cuda.is_available():
         pytest.fail("CUDA device required")
     world, T = 2, 128
