@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--modes", default="cold,classic")
     ap.add_argument("--out", default="")
+    ap.add_argument("--sleep-cycles", type=int, default=400000)
     args = ap.parse_args()
     import torch
     from paper_2505_08944_b200 import amoe
@@ -73,6 +74,9 @@ def main():
                         ctx.token_init(slots, h0[:nt])
                         ctx.enqueue(l, slots, topk_idx=idx, topk_w=wts)
                         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        # keep the stream busy while the host issues the call, so the events bracket
+                        # device time only (not ctypes marshalling / launch latency of an idle GPU)
+                        torch.cuda._sleep(args.sleep_cycles)
                         a.record(stream)
                         ctx.rebatch_ffn_forward(gbs[l])
                         b.record(stream)
