@@ -76,7 +76,17 @@ typedef enum amoe_dtype { AMOE_BF16 = 0, AMOE_FP32 = 1 } amoe_dtype;
  * homed tokens have merged layer l (a box-wide barrier per layer, flags stored into every peer's
  * workspace), which is the dependency an all-to-all before and after each expert layer imposes.
  * Every admitted token must start at the layer of this rank's last amoe_enqueue call. */
-typedef enum amoe_policy { AMOE_DEFRAG = 0, AMOE_MTFS = 1, AMOE_FLFS = 2, AMOE_SYNC = 3 } amoe_policy;
+/* AMOE_DEFRAG_GLOBAL is Algorithm 1 with a box-wide lookahead (PAPER.md
+ * L266-L297 read with Q[l, g] = tokens of layer l on every GPU g, DESIGN.md c11): the picked queue's
+ * own term is this GPU's depth, the lookahead term of block b' sums b' over every rank's queues,
+ * read from the peers' queue counters over NVLink (amoe_run only; identical to AMOE_DEFRAG at G = 1). */
+typedef enum amoe_policy {
+  AMOE_DEFRAG = 0,
+  AMOE_MTFS = 1,
+  AMOE_FLFS = 2,
+  AMOE_SYNC = 3,
+  AMOE_DEFRAG_GLOBAL = 4
+} amoe_policy;
 
 /* Model / placement configuration. */
 typedef struct amoe_config {
@@ -221,6 +231,11 @@ amoe_status amoe_enqueue(amoe_ctx_t ctx, int layer, const int32_t* slots, int T,
  * column q = local queue index (see amoe_local_queue). Synchronises `stream`. */
 amoe_status amoe_queue_depths(amoe_ctx_t ctx, uint32_t* host_out, void* stream);
 
+/* Box-wide depth per block (the AMOE_DEFRAG_GLOBAL lookahead input): host out [L], entry l = queued
+ * legs of layer l summed over every rank's queues, read on device from the peers' queue counters
+ * (amoe_import_peers first when G > 1; EPEER otherwise). Synchronises `stream`. */
+amoe_status amoe_box_depths(amoe_ctx_t ctx, uint32_t* host_out, void* stream);
+
 /* Algorithm 1 / MTFS / FLFS over a host snapshot Q [L * H] (W = lookahead depth, δ = decay;
  * the lookahead divisor N_E is the block's expert count E + S, routed plus shared, box-wide —
  * DESIGN.md reading c11; ties to the smallest (layer, queue)). AMOE_IDLE when all empty.
@@ -232,6 +247,13 @@ amoe_status amoe_pick(amoe_ctx_t ctx, const uint32_t* Q, int policy, int W, floa
  * Returns AMOE_OK with *block/*queue set, AMOE_IDLE when all empty, AMOE_EINVAL on bad args. */
 amoe_status amoe_schedule(const uint32_t* Q, int n_blocks, int n_queues, int n_experts, int policy, int W,
                           float delta, int* block, int* queue);
+
+/* Algorithm 1 with an explicit lookahead (the AMOE_DEFRAG_GLOBAL pick, pure host code): Q_local
+ * [n_blocks * n_queues] = this GPU's hosted depths (the candidates, L283-L286); block_totals
+ * [n_blocks] = queued legs of each block summed over EVERY GPU's queues (the lookahead of
+ * L277-L280), divisor n_experts. AMOE_OK / AMOE_IDLE (every local queue empty) / AMOE_EINVAL. */
+amoe_status amoe_schedule_global(const uint32_t* Q_local, const uint32_t* block_totals, int n_blocks,
+                                 int n_queues, int n_experts, int W, float delta, int* block, int* queue);
 
 /* a4: drain up to max_tokens (0 = all published, also capped by cfg.max_batch and rows_cap)
  * FIFO entries of each queue of `grp` into grp->tile rows (queue q at rows row_off[q] ..

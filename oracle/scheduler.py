@@ -43,6 +43,34 @@ def defrag_scores(Q, W: int = 4, delta: float = 0.5):
     return scores
 
 
+def defrag_global(Q_ranks, rank: int, W: int = 4, delta: float = 0.5, N_E: int | None = None):
+    """Algorithm 1 with the box-wide lookahead (reading c11).
+
+    PAPER.md L268 gives Algorithm 1 the input Q[l, g] — tokens of layer l on GPU g — and L279
+    sums a lookahead block's tokens. Read with g ranging over EVERY GPU of the box (the peers'
+    queue counters are visible over NVLink), the lookahead of block b' is the box-wide total of
+    b' (L279), divided by N_E (L280); the candidates and their own term are this GPU's hosted
+    queues (L283-L286). Q_ranks: [G][N_B][H]; N_E defaults to H (as `defrag`).
+    Argmax ties -> smallest (b, e) block-major (c12). At G = 1 this is `defrag`."""
+    Q = Q_ranks[rank]
+    N_B = len(Q)
+    H = len(Q[0]) if N_B else 0
+    N_E = H if N_E is None else N_E
+    best = None
+    for b in range(N_B):                                   # L274
+        lscore = 0.0                                       # L275
+        for k in range(1, W + 1):                          # L277
+            bp = (b + k) % N_B                             # L278
+            total = float(sum(Qr[bp][ep] for Qr in Q_ranks for ep in range(len(Qr[bp]))))   # L279, every GPU
+            lscore = lscore + (total / N_E) * (delta ** k)       # L280
+        for e in range(H):                                 # L283
+            if Q[b][e] > 0:                                # L285
+                s = lscore + Q[b][e]                       # L286
+                if best is None or s > best[0]:            # L291 argmax
+                    best = (s, b, e)
+    return None if best is None else (best[1], best[2])
+
+
 def mtfs(Q):
     """Most-token-first-serve: the queue with the most tokens; ties -> smallest
     (b, e) in block-major order."""

@@ -13,8 +13,8 @@ import torch
 
 MAX_G, MAX_E, MAX_GROUP = 8, 256, 128
 BF16, FP32 = 0, 1
-DEFRAG, MTFS, FLFS, SYNC = 0, 1, 2, 3
-POLICIES = {"defrag": DEFRAG, "mtfs": MTFS, "flfs": FLFS, "sync": SYNC}
+DEFRAG, MTFS, FLFS, SYNC, DEFRAG_GLOBAL = 0, 1, 2, 3, 4
+POLICIES = {"defrag": DEFRAG, "mtfs": MTFS, "flfs": FLFS, "sync": SYNC, "defrag_global": DEFRAG_GLOBAL}
 BUF = dict(h=0, x=1, pool=2, tok_w=3, tok_idx=4, tok_layer=5, tok_pass=6, rings=7, qctr=8, stats=9, scratch=10,
            tok_time=11)
 STATUS = {0: "OK", 1: "IDLE", 2: "EINVAL", 3: "ENOTHOSTED", 4: "ECUDA", 5: "EDEVICE", 6: "EPEER", 7: "ENOMEM"}
@@ -75,6 +75,9 @@ EXPORTS = {
                             C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "amoe_schedule": (C.c_int, [C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                                 C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "amoe_box_depths": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p]),
+    "amoe_schedule_global": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_float, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "amoe_rebatch": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_int, C.c_void_p]),
     "amoe_expert_ffn": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
     "amoe_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
@@ -173,6 +176,21 @@ def schedule(Q, n_experts, policy="defrag", W=4, delta=0.5):
                               POLICIES[policy], W, delta, C.byref(b), C.byref(e))
     if st not in (0, 1):
         raise AmoeError(st, "amoe_schedule")
+    return None if st == 1 else (b.value, e.value)
+
+
+def schedule_global(Q_local, block_totals, n_experts, W=4, delta=0.5):
+    """Algorithm 1 with a box-wide lookahead (AMOE_DEFRAG_GLOBAL): Q_local [blocks, queues] = this
+    GPU's depths, block_totals [blocks] = every GPU's queued legs per block; None = idle."""
+    import numpy as np
+    q = np.ascontiguousarray(Q_local, dtype=np.uint32)
+    t = np.ascontiguousarray(block_totals, dtype=np.uint32)
+    assert t.shape == (q.shape[0],)
+    b, e = C.c_int(), C.c_int()
+    st = load().amoe_schedule_global(q.ctypes.data_as(C.POINTER(C.c_uint32)), t.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                     q.shape[0], q.shape[1], n_experts, W, delta, C.byref(b), C.byref(e))
+    if st not in (0, 1):
+        raise AmoeError(st, "amoe_schedule_global")
     return None if st == 1 else (b.value, e.value)
 
 
@@ -339,6 +357,13 @@ class Context:
         out = (C.c_uint32 * (self.L * self.H))()
         self._chk(self.lib.amoe_queue_depths(self.h, out, _stream(stream)), "amoe_queue_depths")
         return np.array(out, dtype=np.uint32).reshape(self.L, self.H)
+
+    def box_depths(self, stream=None):
+        """[L] queued legs per layer over every rank's queues (AMOE_DEFRAG_GLOBAL's lookahead)."""
+        import numpy as np
+        out = (C.c_uint32 * self.L)()
+        self._chk(self.lib.amoe_box_depths(self.h, out, _stream(stream)), "amoe_box_depths")
+        return np.array(out, dtype=np.uint32)
 
     def pick(self, Q, policy="defrag", W=4, delta=0.5):
         import numpy as np

@@ -42,6 +42,7 @@ struct Layout {
   uint64_t err;        // u32[8]: code, a0, a1, a2
   uint64_t stats;      // u64[8]: 0 merges, 1 retired, 2 legs executed, 3 legs sent remote
   uint64_t done;       // u32[AMOE_MAX_G]: done epoch per rank (written by that rank)
+  uint64_t gtot;       // u32[L]: box-wide queued legs per block, every rank's queues (AMOE_DEFRAG_GLOBAL)
   uint64_t qctr;       // u32[L*H][4]: reserve, commit, head, pad
   uint64_t rings;      // amoe_leg[L*H][ring_cap]
   uint64_t cctr;       // u32[4]: combine ring reserve, commit, head, pad

@@ -27,7 +27,9 @@ int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUt
 int launch_ffn_cold(const DevCtx&, int, const int*, const int*, int, const CUtensorMap&, const CUtensorMap&, void*, void*,
                     int32_t*, const CUtensorMap*, uint32_t, int, cudaStream_t);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
-int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q);
+int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q,
+               const uint32_t* look = nullptr);
+int launch_peer_depths(const DevCtx&, cudaStream_t);
 }  // namespace amoe
 
 using namespace amoe;
@@ -182,6 +184,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->stats = take(64, 64);
   L->done = take(64, 64);
   L->cctr = take(64, 64);
+  L->gtot = take((uint64_t)c->L * 4, 64);
   L->qctr = take((uint64_t)c->L * H * 16, 64);     // snapshot = [0, qctr end)
   L->rings = take((uint64_t)c->L * H * rc * 16);
   L->cring = take((uint64_t)crc * 16);
@@ -472,6 +475,17 @@ amoe_status amoe_queue_depths(amoe_ctx_t c, uint32_t* host_out, void* stream) {
   return AMOE_OK;
 }
 
+amoe_status amoe_box_depths(amoe_ctx_t c, uint32_t* host_out, void* stream) {
+  if (!c || !host_out) return AMOE_EINVAL;
+  for (int r = 0; r < c->cfg.G; ++r)
+    if (!c->dc.peer[r]) return AMOE_EPEER;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches += launch_peer_depths(c->dc, s);
+  CK(cudaMemcpyAsync(host_out, c->ws + c->lay.gtot, (size_t)c->cfg.L * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return AMOE_OK;
+}
+
 amoe_status amoe_pick(amoe_ctx_t c, const uint32_t* Q, int policy, int W, float delta, int* layer, int* queue) {
   if (!c || !Q || !layer || !queue || policy < 0 || policy > 2 || W < 0) return AMOE_EINVAL;
   return pick_queue(Q, c->cfg.L, c->H, c->cfg.E + c->cfg.S, policy, W, (double)delta, layer, queue) ? AMOE_IDLE
@@ -483,6 +497,12 @@ amoe_status amoe_schedule(const uint32_t* Q, int n_blocks, int n_queues, int n_e
   if (!Q || !block || !queue || n_blocks < 1 || n_queues < 1 || n_experts < 1 || policy < 0 || policy > 2 || W < 0)
     return AMOE_EINVAL;
   return pick_queue(Q, n_blocks, n_queues, n_experts, policy, W, (double)delta, block, queue) ? AMOE_IDLE : AMOE_OK;
+}
+
+amoe_status amoe_schedule_global(const uint32_t* Q, const uint32_t* tot, int n_blocks, int n_queues, int n_experts,
+                                 int W, float delta, int* block, int* queue) {
+  if (!Q || !tot || !block || !queue || n_blocks < 1 || n_queues < 1 || n_experts < 1 || W < 0) return AMOE_EINVAL;
+  return pick_queue(Q, n_blocks, n_queues, n_experts, 0, W, (double)delta, block, queue, tot) ? AMOE_IDLE : AMOE_OK;
 }
 
 static amoe_status make_group(amoe_ctx* c, const amoe_group* g, int max_tokens, GroupDev* gd, int* wslot) {
@@ -775,7 +795,7 @@ static int32_t group_rows(const amoe_ctx* c, const amoe_group& g, int j, const u
 }
 
 amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, amoe_run_stats* stats, void* stream) {
-  if (!c || !p || p->policy < 0 || p->policy > AMOE_SYNC || p->W < 0) return AMOE_EINVAL;
+  if (!c || !p || p->policy < 0 || p->policy > AMOE_DEFRAG_GLOBAL || p->W < 0) return AMOE_EINVAL;
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
   if (!c->dc.router && !c->dc.gate_on) return AMOE_EINVAL;
@@ -863,7 +883,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
     finish(stats);
     return AMOE_EDEVICE;
   };
+  // AMOE_DEFRAG_GLOBAL at G > 1: every poll first reads the box-wide per-block depths from all
+  // ranks' queue counters (peer_depths_kernel -> gtot, inside the snapshot range)
+  const bool global_look = p->policy == AMOE_DEFRAG_GLOBAL && c->cfg.G > 1;
   for (;;) {
+    if (global_look) c->launches += launch_peer_depths(c->dc, s);
     st = snapshot(c, s);   // waits for this rank's previous launches: the GPU is idle from here
     if (st != AMOE_OK) return st;
     const auto t_poll = clk::now();
@@ -937,8 +961,9 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       continue;
     }
     int b = -1, q = -1;
-    const int pol = sync ? AMOE_MTFS : p->policy;
-    bool work = pick_queue(Q.data(), L, H, c->cfg.E + c->cfg.S, pol, p->W, (double)p->delta, &b, &q) == 0;
+    const int pol = sync ? AMOE_MTFS : p->policy == AMOE_DEFRAG_GLOBAL ? AMOE_DEFRAG : p->policy;
+    const uint32_t* look = global_look ? reinterpret_cast<const uint32_t*>(snap + c->lay.gtot) : nullptr;
+    bool work = pick_queue(Q.data(), L, H, c->cfg.E + c->cfg.S, pol, p->W, (double)p->delta, &b, &q, look) == 0;
     if (work && grow_ns > 0) {
       uint64_t depth = 0;
       for (int j = 0; j < H; ++j) depth += Q[(size_t)b * H + j];

@@ -221,6 +221,35 @@ __global__ void __launch_bounds__(kRowThreads) forward_kernel(DevCtx c, GroupDev
   }
 }
 
+// AMOE_DEFRAG_GLOBAL: box-wide queued legs per block, read from every
+// rank's queue counters (peer loads over NVLink; the counters are the same published-minus-
+// drained depths each rank's own scheduler snapshots) into this rank's gtot[L], which the next
+// host snapshot copies. One CTA per block.
+__global__ void peer_depths_kernel(DevCtx c) {
+  AMOE_PDL_ENTRY();
+  const int b = blockIdx.x;
+  uint32_t tot = 0;
+  for (int i = threadIdx.x; i < c.G * c.H; i += blockDim.x) {
+    const int r = i / c.H, q = i - r * c.H;
+    const uint32_t* qc = qctr_ptr(c, r, b * c.H + q);
+    tot += ld_relaxed(qc + 1) - ld_relaxed(qc + 2);
+  }
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  __shared__ uint32_t s_tot[kRowThreads / 32];
+  if ((threadIdx.x & 31) == 0) s_tot[threadIdx.x >> 5] = tot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_tot[w];
+    wsp<uint32_t>(c, c.rank, c.lay.gtot)[b] = t;
+  }
+}
+
+int launch_peer_depths(const DevCtx& c, cudaStream_t s) {
+  launch_pdl(peer_depths_kernel, dim3(c.L), dim3(kRowThreads), 0, s, c);
+  return 1;
+}
+
 int launch_drain(const DevCtx& c, const GroupDev& g, cudaStream_t s) {
   launch_pdl(drain_kernel, dim3(1), dim3(kDrainThreads), 0, s, c, g);
   return 1;

@@ -361,8 +361,41 @@ def test_loopback_peers_match_single_gpu(G, monkeypatch):
     assert remote > 0
 
 
+def test_box_depths_sum_every_rank(monkeypatch):
+    """amoe_box_depths (the AMOE_DEFRAG_GLOBAL lookahead, read on device from the peers' queue
+    counters) equals the per-layer sum of every rank's own queue-depth snapshot, and the oracle's
+    box-wide Algorithm 1 over those snapshots equals the C pick with those totals."""
+    from oracle import scheduler as osch
+    from paper_2505_08944_b200 import amoe as A
+    G, T = 4, 96
+    P = Problem(L=3, E=8, K=2, S=0, d=128, ff=256, T=T, G=G, seed=21)
+    ctxs = [P.make_ctx(rank=r) for r in range(G)]
+    ptrs = [c.ws.data_ptr() for c in ctxs]
+    for c in ctxs:
+        c.import_peers(ptrs)
+    for r, c in enumerate(ctxs):
+        # spread the ranks' tokens over the three layers (rank-dependent split) so blocks differ
+        slots = torch.arange(T, dtype=torch.int32, device="cuda")
+        c.token_init(slots, dev_tensor(P.h0[r], P.dtype), 0)
+        cut = [0, 16 * (r + 1), 16 * (r + 1) + 24, T]
+        for l in range(3):
+            sl = slots[cut[l]:cut[l + 1]]
+            z = torch.from_numpy(np.ascontiguousarray(P.tables[r][0, l][cut[l]:cut[l + 1]])).cuda()
+            c.enqueue(l, sl, logits=z)
+    torch.cuda.synchronize()
+    Qs = [c.queue_depths() for c in ctxs]
+    tot = np.sum([q.sum(axis=1) for q in Qs], axis=0)
+    assert tot.sum() == G * T * P.K
+    for r, c in enumerate(ctxs):
+        got = c.box_depths()
+        assert np.array_equal(got, tot.astype(np.uint32)), (r, got, tot)
+        pick = A.schedule_global(Qs[r], got, P.E, 4, 0.5)
+        assert pick == osch.defrag_global([q.tolist() for q in Qs], r, 4, 0.5, P.E)
+
+
 @pytest.mark.parametrize("G,d,policy,sms", [(2, 128, "defrag", 0), (4, 256, "defrag", 0), (2, 128, "sync", 0),
-                                             (4, 256, "sync", 0), (2, 256, "defrag", 74), (4, 256, "flfs", 36)])
+                                             (4, 256, "sync", 0), (2, 256, "defrag", 74), (4, 256, "flfs", 36),
+                                             (2, 128, "defrag_global", 0), (4, 256, "defrag_global", 36)])
 def test_loopback_amoe_run_concurrent_ranks(G, d, policy, sms, monkeypatch):
     """The native multi-rank loop: G contexts on one GPU, each running amoe_run in its own host
     thread on its own CUDA stream, concurrently. Legs cross ranks through peer rings (remote

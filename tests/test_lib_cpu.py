@@ -61,3 +61,39 @@ def test_host_scheduler_equals_oracle(A, policy):
         d32 = float(np.float32(delta))            # the C ABI takes δ as fp32
         ref = osch.defrag(Ql, W, d32) if policy == "defrag" else osch.POLICIES[policy](Ql)
         assert got == ref, (Ql, W, delta)
+
+
+def test_host_scheduler_global_equals_oracle(A):
+    """AMOE_DEFRAG_GLOBAL's pick (C ABI amoe_schedule_global, the code amoe_run uses) against the
+    oracle's box-wide Algorithm 1 on random multi-rank states; the lookahead totals are summed
+    here from the ranks' depth arrays (what peer_depths_kernel reads from the peers' counters)."""
+    g = np.random.default_rng(11)
+    n_diff = 0
+    for _ in range(2000):
+        G = int(g.choice([1, 2, 4, 8]))
+        NB, NQ, W = int(g.integers(1, 33)), int(g.integers(1, 9)), int(g.integers(0, 6))
+        NE = NQ * G
+        delta = float(np.float32(g.choice([0.5, 0.9, 0.25, 0.7])))
+        Qr = (g.integers(0, 60, (G, NB, NQ)) * (g.random((G, NB, NQ)) < 0.3)).astype(np.uint32)
+        tot = Qr.sum(axis=(0, 2)).astype(np.uint32)
+        for r in range(G):
+            got = A.schedule_global(Qr[r], tot, NE, W, delta)
+            ref = osch.defrag_global(Qr.tolist(), r, W, delta, NE)
+            assert got == ref, (Qr.tolist(), r, W, delta)
+            n_diff += got != osch.defrag([[int(v) for v in row] for row in Qr[r]], W, delta) if got else 0
+    assert n_diff > 0      # the box-wide lookahead changes picks (the test would not see a local fallback)
+
+
+def test_global_oracle_pins():
+    """Pins of defrag_global independent of the C path (hand-executed, W = 1, δ = 0.5, N_E = 2,
+    one queue per block on each of two GPUs; scores = own depth + δ · box-wide total of the next
+    block / N_E):
+    - G = 1 equals Algorithm 1 (`defrag`, itself pinned on SPEC's worked example);
+    - GPU 0 holds [[3], [4]]. Local-only: block 0 = 3 + 0.5·4/2 = 4, block 1 = 4 + 0.5·3/2 = 4.75
+      -> (1, 0). With the peer at [[0], [12]]: block 0 = 3 + 0.5·(4+12)/2 = 7, block 1 = 4.75
+      -> (0, 0): the peer's deep block 1 pulls GPU 0 to the block feeding it;
+    - with the peer at [[9], [0]]: block 0 = 3 + 0.5·4/2 = 4, block 1 = 4 + 0.5·(3+9)/2 = 7 -> (1, 0)."""
+    assert osch.defrag_global([[[5, 0], [3, 2]]], 0, 1, 0.5, 2) == osch.defrag([[5, 0], [3, 2]], 1, 0.5)
+    assert osch.defrag([[3], [4]], 1, 0.5) == (1, 0)
+    assert osch.defrag_global([[[3], [4]], [[0], [12]]], 0, 1, 0.5, 2) == (0, 0)
+    assert osch.defrag_global([[[3], [4]], [[9], [0]]], 0, 1, 0.5, 2) == (1, 0)
