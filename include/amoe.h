@@ -279,6 +279,17 @@ amoe_status amoe_expert_ffn_forward(amoe_ctx_t ctx, const amoe_group* grp, void*
  * amoe_rebatch + amoe_expert_ffn_forward. */
 amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t ctx, const amoe_group* grp, int max_tokens, void* stream);
 
+/* a4 + a5 + a6 + a7 of a COLD pick in ONE launch (small
+ * batches are weight-streaming bound): queue q of `grp` drains exactly n[q] legs (0..128) from ring
+ * position start[q] — the queue's consumer head, as a queue-depth snapshot gives it with
+ * n[q] <= its published depth (the scheduler's decision) — gathers their x rows,
+ * runs the SwiGLU expert and stores every output row into its home's token pool (a7). Writes
+ * grp->qinfo (n, row offset, start); uses grp->act ([nq * n_pad, ff], n_pad = max n rounded up
+ * to 16). bf16 contexts only (EINVAL otherwise). A head that is not start[q] latches device fault
+ * 12 (queue, start, head); an entry never published traps after 4 s (ECUDA). */
+amoe_status amoe_execute_cold(amoe_ctx_t ctx, const amoe_group* grp, const uint32_t* start, const int32_t* n,
+                              void* stream);
+
 /* a7 (return leg): store out rows into pool[home][token_slot][k] (NVLink store when remote),
  * bump the token's leg counter (release, system scope); the leg completing K (+S) appends the
  * token to its home's combine ring. */

@@ -83,6 +83,8 @@ EXPORTS = {
     "amoe_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
     "amoe_expert_ffn_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_void_p]),
     "amoe_rebatch_ffn_forward": (C.c_int, [C.c_void_p, C.POINTER(Group), C.c_int, C.c_void_p]),
+    "amoe_execute_cold": (C.c_int, [C.c_void_p, C.POINTER(Group), C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
+                                    C.c_void_p]),
     "amoe_combine": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "amoe_run": (C.c_int, [C.c_void_p, C.POINTER(RunParams), C.c_int, C.POINTER(RunStats), C.c_void_p]),
     "amoe_pass_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(RunParams),
@@ -386,6 +388,14 @@ class Context:
     def rebatch_ffn_forward(self, gb: GroupBuffers, max_tokens=0, stream=None):
         self._chk(self.lib.amoe_rebatch_ffn_forward(self.h, C.byref(gb.g), max_tokens, _stream(stream)),
                   "amoe_rebatch_ffn_forward")
+
+    def execute_cold(self, gb: GroupBuffers, starts, ns, stream=None):
+        """Fused cold pick: queue q of gb drains exactly ns[q] (<= 128) legs from ring position
+        starts[q] (its consumer head) — amoe_execute_cold."""
+        nq = gb.g.nq
+        st = (C.c_uint32 * nq)(*[int(x) & 0xffffffff for x in starts])
+        n = (C.c_int32 * nq)(*[int(x) for x in ns])
+        self._chk(self.lib.amoe_execute_cold(self.h, C.byref(gb.g), st, n, _stream(stream)), "amoe_execute_cold")
 
     def forward(self, gb: GroupBuffers, stream=None):
         self._chk(self.lib.amoe_forward(self.h, C.byref(gb.g), _stream(stream)), "amoe_forward")

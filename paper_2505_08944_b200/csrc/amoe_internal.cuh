@@ -32,6 +32,7 @@ enum Fault : uint32_t {
   F_PEER_ABORT = 9,       // args: peer rank whose fault (or timeout) aborted this rank's amoe_run (host-latched)
   F_RUN_TIMEOUT = 10,     // args: seconds, merged, expected (host-latched: AMOE_RUN_TIMEOUT expired, G > 1)
   F_LOST_LEG = 11,        // args: stranded token slot, its layer, leg columns returned (host-latched, G == 1)
+  F_HEAD_MISMATCH = 12,   // args: queue, the drain's start position, the queue's consumer head (cold pick)
 };
 // done[] value a faulting rank stores into every peer: never equal to a run epoch
 constexpr uint32_t kAbortEpoch = 0xFFFFFFFFu;
@@ -60,6 +61,7 @@ struct Layout {
   uint64_t tok_idx;    // i32[T][K]
   uint64_t tok_time;   // u64[T][2]: globaltimer (ns) at admission (token_init) and at retirement
   uint64_t wmaps;      // CUtensorMap[L*H][3]
+  uint64_t cmaps;      // CUtensorMap[L*H][4]: K-block views (3-D) W1 x2, W3 x2, W2 x2, W2 x4 (cold kernel)
   uint64_t wptrs;      // u64[L*H][3]
   uint64_t gate;       // u64[L][2]: router gate weights [E][d] (storage dtype) and bias [E] fp32, or 0
   uint64_t s_tile, s_meta, s_qinfo, s_act, s_out;   // amoe_run's group scratch

@@ -24,8 +24,9 @@ int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_forward(const DevCtx&, const GroupDev&, int, cudaStream_t);
 int launch_ffn_tc(const DevCtx&, const FfnLaunch&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                   const CUtensorMap&, void*, void*, const amoe_leg*, int, int, int, cudaStream_t, int);
-int launch_ffn_cold(const DevCtx&, int, const int*, const int*, int, const CUtensorMap&, const CUtensorMap&, void*, void*,
-                    int32_t*, const CUtensorMap*, uint32_t, int, cudaStream_t);
+int launch_ffn_cold(const DevCtx&, int, const int*, const int*, const uint32_t*, int, int, int, const CUtensorMap&, void*,
+                    int32_t*, const CUtensorMap*, const CUtensorMap*, int, cudaStream_t);
+void cold_blocks(int d, int ff, int n_pad, int* ka, int* kb);
 int launch_ffn_simt(const DevCtx&, int, const int32_t*, const int*, const uint64_t*, const void*, void*, void*, int, cudaStream_t);
 int pick_queue(const uint32_t* Q, int NB, int H, int NE, int policy, int W, double delta, int* b, int* q,
                const uint32_t* look = nullptr);
@@ -40,7 +41,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 
 struct MapCacheEntry {
   const void* ptr;
-  int rows, cols, box_rows;
+  int rows, cols, box_rows, depth;
   CUtensorMap map;
 };
 
@@ -75,7 +76,6 @@ struct amoe_ctx {
   // executions logged by amoe_run while profiling: (l*H + q, drained legs), from the ring heads
   std::vector<uint32_t> prev_head;
   std::vector<int32_t> exec_log;
-  uint32_t cold_seq = 0;              // launches of the fused cold kernel (tags its partial flags)
 };
 
 enum Stage { ST_REBATCH = 0, ST_GATEUP = 1, ST_DOWN = 2, ST_FORWARD = 3, ST_COMBINE = 4, ST_ENQUEUE = 5, ST_COLD = 6 };
@@ -123,11 +123,32 @@ static bool encode_bf16_2d(CUtensorMap* m, const void* ptr, int rows, int cols, 
   return r == CUDA_SUCCESS;
 }
 
-static const CUtensorMap* cached_map(amoe_ctx* c, const void* ptr, int rows, int cols, int box_rows) {
+// The same matrix seen as `depth`-deep stacks of K blocks: dims {64, rows, cols/64}, strides
+// {cols*2, 128 B}, box {64, box_rows, depth}. One load lands as `depth` consecutive K-major
+// 128-B-swizzled tiles [kb][box_rows][64] (tools/tma3d_probe.cu checks the layout), so a ring
+// stage needs one TMA box per operand instead of one per K block: a B200 SM retires a roughly
+// fixed number of boxes per microsecond whatever their size up to 32 KB (tools/tma_stream_probe.cu).
+static bool encode_bf16_kb3d(CUtensorMap* m, const void* ptr, int rows, int cols, int box_rows, int depth) {
+  PFN_encodeTiled enc = get_encoder();
+  if (!enc || cols % (64 * depth)) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)depth};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// depth 0: the 2-D map; > 0: the K-block view of that depth
+static const CUtensorMap* cached_map(amoe_ctx* c, const void* ptr, int rows, int cols, int box_rows, int depth = 0) {
   for (auto& e : c->map_cache)
-    if (e.ptr == ptr && e.rows == rows && e.cols == cols && e.box_rows == box_rows) return &e.map;
-  MapCacheEntry e{ptr, rows, cols, box_rows, {}};
-  if (!encode_bf16_2d(&e.map, ptr, rows, cols, box_rows)) return nullptr;
+    if (e.ptr == ptr && e.rows == rows && e.cols == cols && e.box_rows == box_rows && e.depth == depth) return &e.map;
+  MapCacheEntry e{ptr, rows, cols, box_rows, depth, {}};
+  if (depth == 0 ? !encode_bf16_2d(&e.map, ptr, rows, cols, box_rows)
+                 : !encode_bf16_kb3d(&e.map, ptr, rows, cols, box_rows, depth))
+    return nullptr;
   if (c->map_cache.size() > 64) c->map_cache.erase(c->map_cache.begin());
   c->map_cache.push_back(e);
   return &c->map_cache.back().map;
@@ -202,6 +223,7 @@ static void compute_layout(const amoe_config* c, Layout* L, int* Hr_out, uint32_
   L->tok_idx = take(T * c->K * 4);
   L->tok_time = take(T * 16, 16);
   L->wmaps = take((uint64_t)c->L * H * 3 * 128, 128);
+  L->cmaps = take((uint64_t)c->L * H * 4 * 128, 128);
   L->wptrs = take((uint64_t)c->L * H * 3 * 8);
   L->gate = take((uint64_t)c->L * 16);
   L->s_qinfo = take(3 * AMOE_MAX_GROUP * 4);
@@ -367,6 +389,15 @@ amoe_status amoe_set_expert(amoe_ctx_t c, int layer, int expert, const void* w1,
         !encode_bf16_2d(&maps[2], w2, c->cfg.d, c->cfg.ff, 128))
       return AMOE_ECUDA;
     CK(cudaMemcpy(c->ws + c->lay.wmaps + (uint64_t)slot * 3 * 128, maps, sizeof(maps), cudaMemcpyHostToDevice));
+    // K-block views for the cold kernel: W1 / W3 two K blocks deep, W2 two and four (a view
+    // whose depth does not divide the K extent stays zero and is never selected)
+    CUtensorMap cm[4];
+    memset(cm, 0, sizeof(cm));
+    encode_bf16_kb3d(&cm[0], w1, c->cfg.ff, c->cfg.d, 128, 2);
+    encode_bf16_kb3d(&cm[1], w3, c->cfg.ff, c->cfg.d, 128, 2);
+    encode_bf16_kb3d(&cm[2], w2, c->cfg.d, c->cfg.ff, 128, 2);
+    encode_bf16_kb3d(&cm[3], w2, c->cfg.d, c->cfg.ff, 128, 4);
+    CK(cudaMemcpy(c->ws + c->lay.cmaps + (uint64_t)slot * 4 * 128, cm, sizeof(cm), cudaMemcpyHostToDevice));
   }
   for (int i = 0; i < 3; ++i) c->wptrs[(size_t)slot * 3 + i] = ptrs[i];
   c->hosted_flags[slot] = 1;
@@ -620,42 +651,52 @@ static bool cold_enabled() {
   return e && e[0] == '1';
 }
 
-// a4 + a5 + a6 + a7 in ONE launch for a cold pick (k_ffn_cold.cu): drain at most
-// caps[q] legs of each queue, gather, SwiGLU expert, store into the home pools. bf16 only;
-// every cap <= 128; the group's tile / act buffers hold nq * n_pad rows.
-static amoe_status cold_ffn_forward(amoe_ctx* c, const amoe_group* g, const int* caps, cudaStream_t s) {
+// a4 + a5 + a6 + a7 in ONE launch for a cold pick (k_ffn_cold.cu): queue q
+// drains exactly n[q] (<= 128) legs from ring position start[q] (its consumer head, which the
+// scheduler's snapshot gives), gathers, runs the SwiGLU expert, stores into the home pools.
+// bf16 only; the group's act buffer holds nq * n_pad rows.
+static amoe_status cold_ffn_forward(amoe_ctx* c, const amoe_group* g, const int* n, const uint32_t* start,
+                                    cudaStream_t s) {
   GroupDev gd;
   int wslot[AMOE_MAX_GROUP];
   amoe_status st = make_group(c, g, 0, &gd, wslot);
   if (st != AMOE_OK) return st;
-  if (c->cfg.dtype != AMOE_BF16 || !g->act) return AMOE_EINVAL;
+  if (c->cfg.dtype != AMOE_BF16 || !g->act || !n || !start) return AMOE_EINVAL;
   int nmax = 1;
   for (int q = 0; q < g->nq; ++q) {
-    if (caps[q] < 0 || caps[q] > 128) return AMOE_EINVAL;
-    nmax = std::max(nmax, caps[q]);
+    if (n[q] < 0 || n[q] > 128) return AMOE_EINVAL;
+    nmax = std::max(nmax, n[q]);
     if (!c->hosted_flags[wslot[q] / 3]) return AMOE_EINVAL;
   }
   const int n_pad = (nmax + 15) / 16 * 16;
   if ((int64_t)g->nq * n_pad > g->rows_cap) return AMOE_EINVAL;
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
+  int ka = 1, kb = 2;
+  cold_blocks(c->cfg.d, c->cfg.ff, n_pad, &ka, &kb);
   const CUtensorMap* p;
-  CUtensorMap mx, ma;
-  if (!(p = cached_map(c, g->tile, g->rows_cap, c->cfg.d, n_pad))) return AMOE_ECUDA;
-  mx = *p;
-  if (!(p = cached_map(c, g->act, g->rows_cap, c->cfg.ff, n_pad))) return AMOE_ECUDA;
-  ma = *p;
+  if (!(p = cached_map(c, g->act, g->rows_cap, c->cfg.ff, n_pad, kb))) return AMOE_ECUDA;
+  const CUtensorMap ma = *p;
   int qid[AMOE_MAX_GROUP];
   for (int q = 0; q < g->nq; ++q) qid[q] = wslot[q] / 3;
+  int k;
   {
     StageTimer tm(c, ST_COLD, s);
-    c->launches += launch_ffn_cold(c->dc, g->nq, qid, caps, n_pad, mx, ma, g->tile, g->act, g->qinfo,
-                                   reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps), ++c->cold_seq,
-                                   c->num_sms, s);
+    k = launch_ffn_cold(c->dc, g->nq, qid, n, start, n_pad, ka, kb, ma, g->act, g->qinfo,
+                        reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps),
+                        reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.cmaps), c->num_sms, s);
   }
+  if (k < 0) return AMOE_EINVAL;
+  c->launches += k;
   c->last_stream = s;
   CK(cudaGetLastError());
   return AMOE_OK;
+}
+
+amoe_status amoe_execute_cold(amoe_ctx_t c, const amoe_group* g, const uint32_t* start, const int32_t* n,
+                              void* stream) {
+  if (!c || !g || g->nq < 1 || g->nq > AMOE_MAX_GROUP) return AMOE_EINVAL;
+  return cold_ffn_forward(c, g, n, start, (cudaStream_t)stream);
 }
 
 amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_tokens, void* stream) {
@@ -663,13 +704,25 @@ amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_
   cudaStream_t s = (cudaStream_t)stream;
   if (g && g->nq >= 1 && g->nq <= AMOE_MAX_GROUP && g->max_rows_hint >= 1 && g->max_rows_hint <= 128 &&
       c->cfg.dtype == AMOE_BF16 && cold_enabled()) {
-    // cold pick: every queue drains at most the hint (and max_tokens / cfg.max_batch)
+    // cold pick: every queue drains its published depth, at most the hint (and max_tokens /
+    // cfg.max_batch); the heads and depths come from a counter snapshot (synchronises s)
     int cap = g->max_rows_hint;
     if (max_tokens > 0) cap = std::min(cap, max_tokens);
     if (c->cfg.max_batch > 0) cap = std::min(cap, c->cfg.max_batch);
-    int caps[AMOE_MAX_GROUP];
-    for (int q = 0; q < g->nq; ++q) caps[q] = cap;
-    return cold_ffn_forward(c, g, caps, s);
+    GroupDev gd;
+    int wslot[AMOE_MAX_GROUP];
+    amoe_status st = make_group(c, g, 0, &gd, wslot);
+    if (st != AMOE_OK) return st;
+    if ((st = snapshot(c, s)) != AMOE_OK) return st;
+    const uint32_t* qs = c->pinned + c->lay.qctr / 4;
+    int n[AMOE_MAX_GROUP];
+    uint32_t start[AMOE_MAX_GROUP];
+    for (int q = 0; q < g->nq; ++q) {
+      const uint32_t* e = qs + 4 * (wslot[q] / 3);
+      n[q] = (int)std::min<uint32_t>(e[1] - e[2], (uint32_t)cap);
+      start[q] = e[2];
+    }
+    return cold_ffn_forward(c, g, n, start, s);
   }
   // The fused gather is correct (tests) but slower on B200: each A row is re-read by every N tile
   // of its raster group and TMA tile::gather4 moves ~6.6 B/cycle/SM vs >40 for tiled loads
@@ -792,6 +845,12 @@ static void host_latch(amoe_ctx* c, uint32_t code, uint32_t a0, uint32_t a1, uin
 static int32_t group_rows(const amoe_ctx* c, const amoe_group& g, int j, const uint32_t* Q, int H) {
   const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
   return (int32_t)Q[(size_t)g.layer[j] * H + lq];
+}
+
+// consumer head (snapshot) of the group's j-th queue
+static uint32_t group_head(const amoe_ctx* c, const amoe_group& g, int j, int H) {
+  const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
+  return c->pinned[c->lay.qctr / 4 + 4 * ((size_t)g.layer[j] * H + lq) + 2];
 }
 
 amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, amoe_run_stats* stats, void* stream) {
@@ -1013,13 +1072,16 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       // the second drain is stream-ordered behind the first group's forward.
       int n_cold = 0;
       for (int j = 0; j < g.nq; ++j) n_cold += group_rows(c, g, j, Q.data(), H) <= 128;
-      // cold pick: every queue drains <= 128 legs (its snapshot depth, or the max_batch cap)
+      // cold pick: every queue drains <= 128 legs (its snapshot depth, or the max_batch cap),
+      // from its consumer head in the snapshot
       int cold_caps[AMOE_MAX_GROUP];
+      uint32_t cold_start[AMOE_MAX_GROUP];
       bool cold_pick = c->cfg.dtype == AMOE_BF16 && cold_enabled();
       for (int j = 0; j < g.nq && cold_pick; ++j) {
         int cap = group_rows(c, g, j, Q.data(), H);
         if (c->cfg.max_batch > 0) cap = std::min(cap, c->cfg.max_batch);
         cold_caps[j] = cap;
+        cold_start[j] = group_head(c, g, j, H);
         cold_pick = cap <= 128;
       }
       if (split_pick && n_cold > 0 && n_cold < g.nq) {
@@ -1040,7 +1102,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       } else if (cold_pick) {
         // every queue of the pick is cold: the fused one-launch path, each queue drained up to
         // the depth this pick saw (its published prefix at the snapshot)
-        if ((st = cold_ffn_forward(c, &g, cold_caps, s)) != AMOE_OK) return st;
+        if ((st = cold_ffn_forward(c, &g, cold_caps, cold_start, s)) != AMOE_OK) return st;
         rs.picks += 1;
       } else {
         if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;

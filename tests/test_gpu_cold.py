@@ -139,3 +139,46 @@ def test_cold_picks_inside_amoe_run_match_oracle(monkeypatch):
         assert floored_err(h, ref) <= TOL["bf16"]
         assert row_l2_err(h, ref) <= ROW_L2["bf16"]
         ctx.close()
+
+
+def test_execute_cold_explicit_drain_and_head_check():
+    """amoe_execute_cold with the drain made explicit: two enqueue rounds on one queue, the
+    second executed from ring position 37 (the head after draining 37 of the first 60 legs),
+    leaves the other 23 + the new legs queued; a start that is not the head latches fault 12."""
+    from paper_2505_08944_b200 import amoe
+    from paper_2505_08944_b200.amoe import AmoeError
+    P = Problem(L=1, E=1, K=1, S=0, d=256, ff=512, T=120, seed=5, n_tab=1)
+    ctx = P.make_ctx()
+    slots = torch.arange(P.T, dtype=torch.int32, device="cuda")
+    ctx.token_init(slots, dev_tensor(P.h0[0], "bf16"), 0)
+    one = torch.ones(60, 1, device="cuda")
+    zero = torch.zeros(60, 1, dtype=torch.int32, device="cuda")
+    ctx.enqueue(0, slots[:60], topk_idx=zero, topk_w=one)
+    gb = amoe.GroupBuffers(ctx, 512).set_queues([(0, 0)])
+    ctx.execute_cold(gb, [0], [37])
+    torch.cuda.synchronize()
+    ctx.check()
+    assert ctx.queue_depths()[0, 0] == 23
+    ctx.enqueue(0, slots[60:], topk_idx=zero, topk_w=one)
+    ctx.execute_cold(gb, [37], [83])
+    torch.cuda.synchronize()
+    ctx.check()
+    assert ctx.queue_depths()[0, 0] == 0
+    st = ctx.state()
+    assert int(st["stats"][2]) == 120
+    x0 = to_np(st["x"])
+    W = P.W[(0, 0)]
+    pool = to_np(st["pool"])[:, 0]
+    ref = nx.expert_ffn(x0, *W)
+    assert floored_err(pool, ref) <= TOL["bf16"]
+    ctx.combine(retire_pass=1)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert int(ctx.state()["stats"][0]) == 120          # every token merged exactly once
+    # wrong start: the head is 120 now
+    ctx.token_init(slots[:4], dev_tensor(P.h0[0][:4], "bf16"), 0)
+    ctx.enqueue(0, slots[:4], topk_idx=zero[:4], topk_w=one[:4])
+    ctx.execute_cold(gb, [119], [4])
+    with pytest.raises(AmoeError) as ei:
+        ctx.check()
+    assert ei.value.info[:4] == [12, 0, 119, 120]

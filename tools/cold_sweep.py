@@ -7,7 +7,8 @@ Each call is timed alone with CUDA events on its stream (the re-enqueue of the l
 is outside the events); weights rotate over R layers so L2 (126 MB) never holds them. The HBM
 roofline of one call is (6·d·ff weights + 2·n·d token rows in + 2·n·d rows out per expert) / BW,
 the tensor roofline 6·d·ff·n / peak; `frac` = max of the two / measured. AMOE_COLD=1 (default)
-takes the fused one-launch cold kernel for n <= 128; AMOE_COLD=0 the four-kernel path.
+(mode "cold") takes the fused one-launch cold kernel (amoe_execute_cold, n <= 128, the queue
+heads tracked here as the scheduler would); mode "classic" the four-kernel path.
 
     python tools/cold_sweep.py [--shapes mixtral,deepseek] [--groups 1,8] [--ns 1,16,64,128,256,384]
 """
@@ -58,6 +59,7 @@ def main():
                                    torch.empty(d, ff, device="cuda", dtype=torch.bfloat16).normal_(0, ff ** -0.5, generator=gen))
             h0 = torch.randn(Gx * nmax, d, device="cuda", dtype=torch.bfloat16)
             gbs = [amoe.GroupBuffers(ctx, Gx * ((nmax + 255) // 256) * 256 + 256) for _ in range(R)]
+            heads = [0] * R                    # consumer head of every queue of layer l (all advance together)
             for n in ns:
                 nt = n * Gx
                 slots = torch.arange(nt, dtype=torch.int32, device="cuda")
@@ -65,6 +67,8 @@ def main():
                 wts = torch.ones(nt, 1, device="cuda")
                 for mode in args.modes.split(","):
                     os.environ["AMOE_COLD"] = "1" if mode == "cold" else "0"
+                    if mode == "cold" and n > 128:
+                        continue
                     for g, l in zip(gbs, range(R)):
                         g.set_queues([(l, e) for e in range(Gx)], max_rows_hint=n)
                     evs = []
@@ -78,7 +82,12 @@ def main():
                         # device time only (not ctypes marshalling / launch latency of an idle GPU)
                         torch.cuda._sleep(args.sleep_cycles)
                         a.record(stream)
-                        ctx.rebatch_ffn_forward(gbs[l])
+                        if mode == "cold":
+                            # the scheduler's decision made explicit: each queue's head and depth
+                            ctx.execute_cold(gbs[l], [heads[l]] * Gx, [n] * Gx)
+                        else:
+                            ctx.rebatch_ffn_forward(gbs[l])
+                        heads[l] += n
                         b.record(stream)
                         if i >= 2:
                             evs.append((a, b))

@@ -5,9 +5,9 @@
     AMOE_LIB=_ab/libamoe_ctrace.so python tools/cold_trace.py --shape deepseek --experts 1 --n 1
 
 Stamps (globaltimer ns, relative to the earliest CTA entry): 0 entry, 1 producer past the grid
-dependency, 2 drain flag seen, 3 gather arrival, 4 first token-tile load issued, 5 last gate/up
-MMA issued, 6 gate/up epilogues done, 7 gate/up reductions done, 8 first act load issued,
-9 MMA done, 10 down reductions done, 11 exit. Prints min / median / max over CTAs.
+dependency, 2 producer done, 3 MMA issuer done, 4 first gather table loaded, 5 a gate/up split
+reduced here (last arriver), 6 a down split reduced here, 7 gate/up epilogues done, 8 down
+epilogues done, 11 exit. Prints min / median / max / count over CTAs.
 """
 import argparse
 import ctypes as C
@@ -19,8 +19,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-NAMES = ["entry", "griddep", "drain_seen", "gather_done", "first_B", "mmaA_done", "epiA_done", "redA_done",
-         "first_actB", "mma_done", "redB_done", "exit", "lastA_tfull", "redA_flags", "redB_flags", "-"]
+NAMES = ["entry", "griddep", "producer_done", "mma_done", "gather_table", "redA_last", "redB_last", "epiA_done",
+         "epiB_done", "-", "-", "exit", "W:prod_empty", "W:mma_full", "W:gather_empty", "W:gather_cpasync"]
 
 
 def main():
@@ -70,7 +70,7 @@ def main():
     out = {"shape": args.shape, "experts": Gx, "n": n, "ctas": P, "event_us": round(ms * 1e3, 2), "points_us": {}}
     for i, name in enumerate(NAMES):
         v = tr[i][used]
-        v = v[v > 0] - t0
+        v = v[v > 0] - (0 if name.startswith("W:") else t0)
         if v.size:
             out["points_us"][name] = [round(float(v.min()) / 1e3, 2), round(float(np.median(v)) / 1e3, 2),
                                       round(float(v.max()) / 1e3, 2), int(v.size)]
