@@ -644,11 +644,23 @@ amoe_status amoe_expert_ffn_forward(amoe_ctx_t c, const amoe_group* g, void* str
   return expert_ffn(c, g, 1, (cudaStream_t)stream);
 }
 
-// The fused cold path (AMOE_COLD=1) vs the four-kernel path (default while the fused kernel is
-// being tuned: profiles/r02_cold_sweep.md).
-static bool cold_enabled() {
+// The fused cold path (k_ffn_cold.cu) vs the four-kernel path for a pick whose queues hold at
+// most n_max legs each (nq queues): AMOE_COLD=1 forces the fused kernel (n_max <= 128), 0 the
+// four-kernel path; by default the fused kernel takes the picks where it measured faster
+// (profiles/r02_cold_sweep.md, device time per pick on one B200):
+//  * n_max <= 16: every shape (weight streaming dominates; one launch, no grid-wide hand-off);
+//  * n_max <= 32: unless the pick streams more than 1 GB of weights (Mixtral-sized groups);
+//  * n_max <= 64: DeepSeek-sized experts (d <= 2048) in groups of >= 4.
+static bool cold_pick_ok(const amoe_ctx* c, int n_max, int nq) {
+  if (c->cfg.dtype != AMOE_BF16 || n_max < 1 || n_max > 128) return false;
   const char* e = getenv("AMOE_COLD");
-  return e && e[0] == '1';
+  if (e && e[0] == '1') return true;
+  if (e && e[0] == '0') return false;
+  const double wbytes = 6.0 * c->cfg.d * c->cfg.ff * nq;
+  if (n_max <= 16) return true;
+  if (n_max <= 32) return wbytes <= 1e9;
+  if (n_max <= 64) return c->cfg.d <= 2048 && nq >= 4;
+  return false;
 }
 
 // a4 + a5 + a6 + a7 in ONE launch for a cold pick (k_ffn_cold.cu): queue q
@@ -702,8 +714,7 @@ amoe_status amoe_execute_cold(amoe_ctx_t c, const amoe_group* g, const uint32_t*
 amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_tokens, void* stream) {
   if (!c) return AMOE_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (g && g->nq >= 1 && g->nq <= AMOE_MAX_GROUP && g->max_rows_hint >= 1 && g->max_rows_hint <= 128 &&
-      c->cfg.dtype == AMOE_BF16 && cold_enabled()) {
+  if (g && g->nq >= 1 && g->nq <= AMOE_MAX_GROUP && cold_pick_ok(c, g->max_rows_hint, g->nq)) {
     // cold pick: every queue drains its published depth, at most the hint (and max_tokens /
     // cfg.max_batch); the heads and depths come from a counter snapshot (synchronises s)
     int cap = g->max_rows_hint;
@@ -1076,14 +1087,15 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       // from its consumer head in the snapshot
       int cold_caps[AMOE_MAX_GROUP];
       uint32_t cold_start[AMOE_MAX_GROUP];
-      bool cold_pick = c->cfg.dtype == AMOE_BF16 && cold_enabled();
-      for (int j = 0; j < g.nq && cold_pick; ++j) {
+      int cold_max = 0;
+      for (int j = 0; j < g.nq; ++j) {
         int cap = group_rows(c, g, j, Q.data(), H);
         if (c->cfg.max_batch > 0) cap = std::min(cap, c->cfg.max_batch);
         cold_caps[j] = cap;
         cold_start[j] = group_head(c, g, j, H);
-        cold_pick = cap <= 128;
+        cold_max = std::max(cold_max, cap);
       }
+      const bool cold_pick = cold_pick_ok(c, cold_max, g.nq);
       if (split_pick && n_cold > 0 && n_cold < g.nq) {
         amoe_group gc = g, gh = g;
         gc.nq = gh.nq = 0;

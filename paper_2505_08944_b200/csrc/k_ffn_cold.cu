@@ -219,6 +219,7 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
     s_legq = -1;
 #ifdef AMOE_COLD_TRACE
     for (int i = 12; i < 16; ++i) g_cold_trace[i][blockIdx.x] = 0;
+    g_cold_trace[9][blockIdx.x] = 0;
 #endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -346,7 +347,9 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
         it.get(j, ph, t, k);
         const bool first = it.seg_first(j), last = it.seg_last(j);
         if (first) {
+          CW_BEGIN();
           mbar_wait_wd(smem_u32(&bars[2 * MAXS + 2 + acc]), acc_phase ^ 1u, 2);
+          CW_END(9);
           tc_fence_after();
         }
         const uint32_t d0 = tmem_base + (uint32_t)(acc * 256);
@@ -356,9 +359,15 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
           CW_END(13);
         }
         tc_fence_after();
+#ifndef AMOE_COLD_NOPROXY   // diagnostic only
         if (ph == 0) proxy_fence_smem();   // the gathered leg rows (cp.async, generic proxy) -> tensor core
+#endif
         const uint32_t sa = smem_u32(ring + stage * stage_bytes);
+#ifdef AMOE_COLD_NOMMA   // diagnostic only: wrong results
+        if (false) {
+#else
         if (ph == 0) {
+#endif
           for (int kb = 0; kb < KA; ++kb) {
             const uint64_t a0d = umma_desc_sw128(sa + kb * A_BYTES), a1d = umma_desc_sw128(sa + (KA + kb) * A_BYTES);
             const uint64_t b0d = umma_desc_sw128(sa + 2 * KA * A_BYTES + kb * n_pad * 128);
@@ -369,7 +378,11 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
               umma_bf16(d0 + (uint32_t)n_pad, a1d + 2 * kk, b0d + 2 * kk, idesc, accum);  // up
             }
           }
-        } else {
+        } else
+#ifdef AMOE_COLD_NOMMA
+        if (false)
+#endif
+        {
           for (int kb = 0; kb < KB; ++kb) {
             const uint64_t a0d = umma_desc_sw128(sa + kb * A_BYTES);
             const uint64_t b0d = umma_desc_sw128(sa + KB * A_BYTES + kb * n_pad * 128);
@@ -447,7 +460,11 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
 #pragma unroll
         for (int u = 0; u < MAXC; ++u) {
           const int r = 4 * u + (lane >> 3), c = lane & 7, i = gw * 64 + r;
+#ifdef AMOE_COLD_NOGATHER   // diagnostic only: wrong results
+          if (false)
+#else
           if (r < nq_rows)
+#endif
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
                          :: "r"(sb + kb * n_pad * 128 + i * 128 + ((c ^ (i & 7)) * 16)),
                             "l"(rp[u] + (uint64_t)(KA * k + kb) * 128) : "memory");
@@ -712,6 +729,15 @@ extern "C" amoe_status amoe_debug_cold_trace(unsigned long long* out) {
 // divides the K extents (d / 64, ff / 64). Deeper iterations mean fewer TMA boxes per byte.
 void cold_blocks(int d, int ff, int n_pad, int* ka, int* kb) {
   using namespace cold;
+  if (const char* e = getenv("AMOE_COLD_KAKB")) {   // A/B override "ka,kb" (profiles/r02_cold_sweep.md)
+    int x = 0, y = 0;
+    if (sscanf(e, "%d,%d", &x, &y) == 2 && (x == 1 || x == 2) && (y == 2 || y == 4) && (d / 64) % x == 0 &&
+        (ff / 64) % y == 0) {
+      *ka = x;
+      *kb = y;
+      return;
+    }
+  }
   const int cand[3][2] = {{2, 4}, {2, 2}, {1, 2}};
   for (const auto& ck : cand) {
     const int sb = std::max(ck[0] * (2 * A_BYTES + n_pad * 128), ck[1] * (A_BYTES + n_pad * 128));
@@ -769,7 +795,7 @@ int launch_ffn_cold(const DevCtx& c, int nq, const int* qid, const int* n, const
   static int red_kb = -1;
   if (red_kb < 0) {
     const char* e = getenv("AMOE_COLD_RED_KB");
-    red_kb = e ? std::max(1, atoi(e)) : 512;
+    red_kb = e ? std::max(1, atoi(e)) : 64;
   }
   const int cap_sms = std::min(num_sms, MAXP);
   auto plan = [&](int tiles, int ipt, int width) {

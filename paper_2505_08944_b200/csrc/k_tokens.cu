@@ -20,6 +20,16 @@ constexpr int kTPC = kTokWarps * kTPW;        // tokens per CTA chunk
 // both slower (Mixtral combine 225 -> 268 -> 458 us/layer): parallelism comes from warps.
 constexpr int kU = 1;
 
+// Tokens one CTA takes per chunk of an n-token launch: kTPC (kTPW per warp) when the grid has
+// that much work, else a multiple of the warp count spread over the grid so a warp merges at most
+// one token — a small merge is one latency chain per token, not kTPW of them in a row (the
+// combine after a cold pick of a few dozen tokens: profiles/r02_combine_small.md).
+__device__ __forceinline__ int chunk_tokens(int n) {
+  int tpc = (n + (int)gridDim.x - 1) / (int)gridDim.x;
+  tpc = (tpc + kTokWarps - 1) / kTokWarps * kTokWarps;
+  return tpc < kTokWarps ? kTokWarps : (tpc > kTPC ? kTPC : tpc);
+}
+
 struct PendingLeg {
   int32_t r;      // owner rank (-1 = inactive)
   int32_t q;      // queue index on the owner
@@ -249,13 +259,16 @@ __global__ void __launch_bounds__(kTokThreads) enqueue_kernel(DevCtx c, int laye
   AMOE_PDL_ENTRY();
   __shared__ PendingLeg legs[kTPC * kMaxKS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int chunk = blockIdx.x; chunk * kTPC < n; chunk += gridDim.x) {
+  // tokens per CTA chunk: a full chunk (kTPC) when there are enough tokens, otherwise spread so
+  // every warp of the grid takes at most one token (few tokens: one latency chain, not kTPW)
+  const int tpc = chunk_tokens(n);
+  for (int base = blockIdx.x * tpc; base < n; base += gridDim.x * tpc) {
     for (int t = 0; t < kTPW; ++t) {
-      const int lt = warp * kTPW + t;
-      const int i = chunk * kTPC + lt;
+      const int lt = t * kTokWarps + warp;
+      const int i = base + lt;
       PendingLeg* my = legs + lt * c.KS;
       if (lane < c.KS) my[lane].r = -1;
-      if (i >= n) continue;
+      if (lt >= tpc || i >= n) continue;
       const int slot = slots[i];
       if (slot < 0 || slot >= c.T) { if (lane == 0) raise_fault(c, F_SLOT_RANGE, slot, c.T, 1); continue; }
       int my_e = -1;
@@ -400,14 +413,15 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
   if (threadIdx.x == 0) { s_merged = 0; s_retired = 0; }
   __syncthreads();
   const bool gate_tc = GATE && c.dtype == AMOE_BF16 && (c.E % 8) == 0;
-  for (int chunk = blockIdx.x; chunk * kTPC < n; chunk += gridDim.x) {
+  const int tpc = chunk_tokens(n);
+  for (int base = blockIdx.x * tpc; base < n; base += gridDim.x * tpc) {
     for (int t = 0; t < kTPW; ++t) {
-      const int lt = warp * kTPW + t;
-      const int i = chunk * kTPC + lt;
+      const int lt = t * kTokWarps + warp;
+      const int i = base + lt;
       PendingLeg* my = legs + lt * c.KS;
       if (lane < c.KS) my[lane].r = -1;
       if (GATE && lane == 0) s_gslot[lt] = -1;
-      if (i >= n) continue;
+      if (lt >= tpc || i >= n) continue;
       const uint32_t pos = start + (uint32_t)i;
       const amoe_leg e = ring[pos & c.cring_mask];
       if (e.seq != pos + 1u) { if (lane == 0) raise_fault(c, F_STALE_ENTRY, 0xffffffffu, pos, e.seq); continue; }
@@ -511,7 +525,7 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
       __syncthreads();
       if (u != -2) {
         for (int t = 0; t < kTPW; ++t) {
-          const int lt = warp * kTPW + t;
+          const int lt = t * kTokWarps + warp;
           const int slot = s_gslot[lt];
           if (slot < 0) continue;
           const int layer = s_glayer[lt], pass = s_gpass[lt];
@@ -574,7 +588,7 @@ int launch_token_init(const DevCtx& c, const int32_t* slots, int n, const void* 
 int launch_enqueue(const DevCtx& c, int layer, const int32_t* slots, int n, const float* logits,
                    const int32_t* tidx, const float* tw, cudaStream_t s) {
   if (n <= 0) return 0;
-  int grid = (n + kTPC - 1) / kTPC;
+  int grid = (n + kTokWarps - 1) / kTokWarps;     // chunk_tokens: one token per warp when few
   if (grid > 1184) grid = 1184;
   launch_pdl(enqueue_kernel, dim3(grid), dim3(kTokThreads), 0, s, c, layer, slots, n, logits, tidx, tw);
   return 1;

@@ -100,7 +100,8 @@ def main():
                     r = {"shape": shape, "experts": Gx, "n": n, "mode": mode, "us": round(t * 1e6, 2),
                          "weight_gbs": round(wbytes_expert * Gx / t / 1e9, 1), "roofline_us": round(roof * 1e6, 2),
                          "frac": round(roof / t, 3), "bound": "tensor" if flop / tc > byts / hbm else "hbm",
-                         "path": "cold fused (1 launch)" if (mode == "cold" and n <= 128) else "drain+gather+gateup+down"}
+                         "path": "cold fused (1 launch)" if (mode == "cold" and n <= 128) else "drain+gather+gateup+down",
+                         "kakb": os.environ.get("AMOE_COLD_KAKB", "auto")}
                     print(json.dumps(r), flush=True)
                     rows.append(r)
             ctx.close()

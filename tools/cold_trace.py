@@ -20,7 +20,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 NAMES = ["entry", "griddep", "producer_done", "mma_done", "gather_table", "redA_last", "redB_last", "epiA_done",
-         "epiB_done", "-", "-", "exit", "W:prod_empty", "W:mma_full", "W:gather_empty", "W:gather_cpasync"]
+         "epiB_done", "W:mma_tempty", "-", "exit", "W:prod_empty", "W:mma_full", "W:gather_empty", "W:gather_cpasync"]
 
 
 def main():

@@ -13,7 +13,7 @@ for l in open('gpurun_out/cold_sweep4.log'):
     print(r['shape'],r['experts'],r['n'],r['mode'],r['us'],r['frac'])
 PY
 python -m paper_2505_08944_b200.build --out _ab/libamoe_ctrace.so --flags=-DAMOE_COLD_TRACE > gpurun_out/build_ctrace.log 2>&1
-for cfg in "deepseek 1 1" "deepseek 8 1" "deepseek 8 64" "mixtral 1 1" "mixtral 8 1"; do
+for cfg in ${TRACE_CFGS:-"deepseek 1 1" "deepseek 8 1" "deepseek 8 64" "mixtral 1 1" "mixtral 8 1"}; do
   set -- $cfg
   AMOE_COLD=1 AMOE_LIB=_ab/libamoe_ctrace.so timeout 120 python tools/cold_trace.py --shape $1 --experts $2 --n $3 2>&1 | tail -1
 done > gpurun_out/cold_trace4.log
