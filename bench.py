@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--router", default="table", choices=["table", "gate"],
                     help="table: synthetic Zipf logits (the paper's eval); gate: device router gate "
                          "x·Wgᵀ + per-layer Zipf log-prob bias computed in the combine (SURVEY.md f3)")
+    ap.add_argument("--topk", type=int, default=0, help="override top-K (1: the paper's Top-1 routing, P:L463)")
+    ap.add_argument("--direct", action="store_true",
+                    help="top-1 direct forwarding (amoe_set_direct; needs --topk 1): the executing rank "
+                         "merges and routes each token itself, no token pool / combine launch (SURVEY.md f3)")
     ap.add_argument("--skew", default="zipf", choices=["zipf", "exp"],
                     help="routing skew: Zipf s=1.2 (BASELINE.json) or the paper's exponential fit (λ=0.38)")
     return ap.parse_args()
@@ -59,14 +63,15 @@ def FFN_KERNEL(d):
     return "ffn_tc_kernel<GATEUP> (tcgen05 UMMA 128x256, fused SwiGLU)"
 
 
-def config_dict(spec, L, T, G, policy, grouped, skew="zipf", router="table"):
+def config_dict(spec, L, T, G, policy, grouped, skew="zipf", router="table", direct=False):
     """The workload description shared by both arms' JSON lines."""
     return {"workload": f"{spec.name}-shaped expert layers: L={L} E={spec.E} top-{spec.K} S={spec.S} d={spec.d} "
                         f"ff={spec.ff}, {T} tokens in flight per GPU, "
                         + (f"Zipf s={spec.zipf_s}" if skew == "zipf" else "exponential λ=0.38") + " routing",
             "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped, "router": router,
             "l2": "inputs larger than L2 (resident weights >> 126 MB); no flush",
-            "step": "one decode pass: every token through all L layers"}
+            "step": "one decode pass: every token through all L layers",
+            "merge": "direct top-1 forwarding on the executing rank" if direct else "token pool + combine on the home"}
 
 
 def peaks_bf16():
@@ -312,6 +317,9 @@ def main():
             dist.init_process_group(backend)
     cdev = dev if backend == "nccl" else "cpu"       # device of the timing / stall reductions
     spec = wl.CONFIGS[args.config]
+    if args.topk:
+        import dataclasses
+        spec = dataclasses.replace(spec, K=args.topk)
     L = args.L or spec.L
     T = args.T or spec.T
     E, K, S, d, ff = spec.E, spec.K, spec.S, spec.d, spec.ff
@@ -341,6 +349,8 @@ def main():
                    for p in range(n_tab)]
     table = torch.from_numpy(np.stack(tables_host)).to(dev).contiguous()
     ctx.set_router(table)
+    if args.direct:
+        ctx.set_direct(True)
     gate_w = []
     if args.router == "gate":
         for l in range(L):
@@ -455,7 +465,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
-        "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router),
+        "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router, args.direct),
         "gpu_launches": int(launches),
         "die_map_sms": list(amoe.die_info()),
         "clocks": clk,

@@ -231,6 +231,15 @@ amoe_status amoe_enqueue(amoe_ctx_t ctx, int layer, const int32_t* slots, int T,
  * column q = local queue index (see amoe_local_queue). Synchronises `stream`. */
 amoe_status amoe_queue_depths(amoe_ctx_t ctx, uint32_t* host_out, void* stream);
 
+/* Top-1 direct forwarding (PAPER.md L463 — with one expert per token there is
+ * no top-K merge to wait for; L227-L228 — a token ready by itself skips the token pool): when on,
+ * amoe_run's executing rank merges each token it ran (h += w·O, the combine's arithmetic),
+ * normalises it, routes its next layer and scatters the next leg straight into that expert's queue;
+ * the home's pool, leg counter, combine ring and combine launch are not used. Requires K == 1 and
+ * S == 0 (EINVAL otherwise); at G > 1 every layer must route with a gate (amoe_set_gate, checked
+ * by amoe_run: EINVAL). Results equal the pooled path bit for bit. */
+amoe_status amoe_set_direct(amoe_ctx_t ctx, int on);
+
 /* Box-wide depth per block (the AMOE_DEFRAG_GLOBAL lookahead input): host out [L], entry l = queued
  * legs of layer l summed over every rank's queues, read on device from the peers' queue counters
  * (amoe_import_peers first when G > 1; EPEER otherwise). Synchronises `stream`. */

@@ -75,6 +75,7 @@ EXPORTS = {
                             C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "amoe_schedule": (C.c_int, [C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                                 C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "amoe_set_direct": (C.c_int, [C.c_void_p, C.c_int]),
     "amoe_box_depths": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p]),
     "amoe_schedule_global": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_int,
                                        C.c_int, C.c_float, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -359,6 +360,10 @@ class Context:
         out = (C.c_uint32 * (self.L * self.H))()
         self._chk(self.lib.amoe_queue_depths(self.h, out, _stream(stream)), "amoe_queue_depths")
         return np.array(out, dtype=np.uint32).reshape(self.L, self.H)
+
+    def set_direct(self, on=True):
+        """Top-1 direct forwarding (amoe_set_direct; K == 1, S == 0)."""
+        self._chk(self.lib.amoe_set_direct(self.h, 1 if on else 0), "amoe_set_direct")
 
     def box_depths(self, stream=None):
         """[L] queued legs per layer over every rank's queues (AMOE_DEFRAG_GLOBAL's lookahead)."""

@@ -18,6 +18,7 @@ int launch_token_init(const DevCtx&, const int32_t*, int, const void*, int, cuda
 int launch_enqueue(const DevCtx&, int, const int32_t*, int, const float*, const int32_t*, const float*, cudaStream_t);
 int launch_combine(const DevCtx&, int, int, cudaStream_t);
 int launch_announce(const DevCtx&, uint32_t, int, cudaStream_t);
+int launch_direct_merge(const DevCtx&, const GroupDev&, int, int, cudaStream_t);
 int die_map(uint64_t mask[4], int counts[2]);
 int launch_drain(const DevCtx&, const GroupDev&, cudaStream_t);
 int launch_gather(const DevCtx&, const GroupDev&, int, cudaStream_t);
@@ -47,6 +48,7 @@ struct MapCacheEntry {
 
 struct amoe_ctx {
   amoe_config cfg;
+  bool direct = false;                // top-1 direct forwarding (amoe_set_direct)
   DevCtx dc;
   Layout lay;
   char* ws;
@@ -414,6 +416,13 @@ amoe_status amoe_set_gate(amoe_ctx_t c, int layer, const void* wg, const float* 
   c->gate_set[layer] = wg != nullptr;
   c->dc.gate_on = 0;
   for (char g : c->gate_set) c->dc.gate_on |= g;
+  return AMOE_OK;
+}
+
+amoe_status amoe_set_direct(amoe_ctx_t c, int on) {
+  if (!c) return AMOE_EINVAL;
+  if (on && (c->cfg.K != 1 || c->cfg.S != 0)) return AMOE_EINVAL;
+  c->direct = on != 0;
   return AMOE_OK;
 }
 
@@ -869,6 +878,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   for (int r = 0; r < c->cfg.G; ++r)
     if (!c->dc.peer[r]) return AMOE_EPEER;
   if (!c->dc.router && !c->dc.gate_on) return AMOE_EINVAL;
+  if (c->direct && c->cfg.G > 1) {
+    // direct forwarding at G > 1 routes with the router gate: every layer needs one here
+    for (int l = 0; l < c->cfg.L; ++l)
+      if ((int)c->gate_set.size() < c->cfg.L || !c->gate_set[l]) return AMOE_EINVAL;
+  }
   for (size_t i = 0; i < c->hosted_flags.size(); ++i)
     if (!c->hosted_flags[i]) {
       // every hosted queue needs weights (routed experts of this rank and the shared experts)
@@ -1111,6 +1125,19 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         if ((st = amoe_rebatch_ffn_forward(c, &gc, 0, s)) != AMOE_OK) return st;
         if ((st = amoe_rebatch_ffn_forward(c, &gh, 0, s)) != AMOE_OK) return st;
         rs.picks += 1;   // one pick, two launches
+      } else if (c->direct) {
+        // top-1 direct forwarding (f3): drain + gather, SwiGLU expert into the group's out rows,
+        // then this rank merges, normalises, routes and scatters each token itself
+        if ((st = amoe_rebatch(c, &g, 0, s)) != AMOE_OK) return st;
+        if ((st = expert_ffn(c, &g, 0, s)) != AMOE_OK) return st;
+        GroupDev gd;
+        if ((st = make_group(c, &g, 0, &gd, nullptr)) != AMOE_OK) return st;
+        {
+          StageTimer tm(c, ST_COMBINE, s);
+          c->launches += launch_direct_merge(c->dc, gd, retire_pass, c->num_sms, s);
+        }
+        CK(cudaGetLastError());
+        rs.picks += 1;
       } else if (cold_pick) {
         // every queue of the pick is cold: the fused one-launch path, each queue drained up to
         // the depth this pick saw (its published prefix at the snapshot)
@@ -1120,7 +1147,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;
         rs.picks += 1;
       }
-      if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
+      if (!c->direct && (st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
       rs.kernel_launches += c->launches - l0;
       rs.queues_run += g.nq;
       idle_streak = 0;

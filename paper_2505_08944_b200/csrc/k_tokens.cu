@@ -564,6 +564,164 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
   }
 }
 
+// ---------------------------------------------------------------------------- direct merge (f3)
+// Top-1 direct forwarding (with one expert per token there
+// is no top-K merge to wait for, L227-L228: a token that is ready by itself skips the token
+// pool). With K = 1 and no shared experts the rank that executed a token's leg merges it
+// itself, right after the FFN: h ← store(h + w·O) (the combine's arithmetic, no FMA), x =
+// RMSNorm(h) written back to the token's home, the next layer routed and the new leg scattered
+// straight into the next expert's queue — no pool row, no leg counter, no combine ring, no merge
+// launch on the home. The FFN output rows are this rank's group `out` rows; h, x and the token
+// state stay on the home (NVLink peer loads/stores when remote). Routing: the router gate of
+// the next layer (any G), or the router table (G = 1: the table is this rank's).
+template <typename T, bool GATE>
+__global__ void __launch_bounds__(kTokThreads) direct_merge_kernel(DevCtx c, GroupDev g, int retire_pass) {
+  AMOE_PDL_ENTRY();
+  using V = Vec<T>;
+  __shared__ PendingLeg legs[kTPC * kMaxKS];
+  __shared__ int pre[AMOE_MAX_GROUP + 1];
+  __shared__ unsigned long long s_legs, s_remote;
+  __shared__ int s_home[kTPC];                 // home of the token merged at chunk position lt (-1: none)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int q = 0; q < g.nq; ++q) { pre[q] = acc; acc += g.qinfo[q]; }
+    pre[g.nq] = acc;
+    s_legs = 0; s_remote = 0;
+  }
+  __syncthreads();
+  const int n = pre[g.nq];
+  const bool sys = c.G > 1;
+  const int tpc = chunk_tokens(n);
+  for (int base = blockIdx.x * tpc; base < n; base += gridDim.x * tpc) {
+    for (int t = 0; t < kTPW; ++t) {
+      const int lt = t * kTokWarps + warp;
+      const int i = base + lt;
+      PendingLeg* my = legs + lt * c.KS;
+      if (lane < c.KS) my[lane].r = -1;
+      if (lane == 0) s_home[lt] = -1;
+      if (lt >= tpc || i >= n) continue;
+      int q = 0;
+      while (q + 1 < g.nq && pre[q + 1] <= i) ++q;
+      const int row = g.qinfo[AMOE_MAX_GROUP + q] + (i - pre[q]);
+      const amoe_leg e = g.meta[row];
+      const int home = e.home, slot = e.token_slot;
+      if (home < 0 || home >= c.G || slot < 0 || slot >= c.T) {
+        if (lane == 0) raise_fault(c, F_STALE_ENTRY, 0xfffffffeu, (uint32_t)row, e.seq);
+        continue;
+      }
+      int32_t* tlayer = reinterpret_cast<int32_t*>(c.peer[home] + c.lay.tok_layer);
+      int32_t* tpass = reinterpret_cast<int32_t*>(c.peer[home] + c.lay.tok_pass);
+      int layer = tlayer[slot] + 1;
+      int pass = tpass[slot];
+      if (layer == c.L) { layer = 0; ++pass; }
+      const bool retire = pass >= retire_pass;
+      float zv[kZJ];
+      const T* gw = nullptr;
+      const float* gb = nullptr;
+      if (GATE && !retire) {
+        const uint64_t* ge = gate_entry(c, layer);
+        gw = reinterpret_cast<const T*>(ge[0]);
+        gb = reinterpret_cast<const float*>(ge[1]);
+      }
+      if (!retire && c.router && !gw)
+        route_load(c.router + (((uint64_t)(pass % c.n_tab) * c.L + layer) * c.T + slot) * c.E, c.E, lane, zv);
+      T* h = reinterpret_cast<T*>(c.peer[home] + c.lay.h) + (uint64_t)slot * c.d;
+      T* x = reinterpret_cast<T*>(c.peer[home] + c.lay.x) + (uint64_t)slot * c.d;
+      const T* orow = reinterpret_cast<const T*>(g.out) + (uint64_t)row * c.d;
+      const float wk = e.w;
+      float ss = 0.f;
+      for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
+        const uint4 hraw = *reinterpret_cast<const uint4*>(h + col);
+        const uint4 oraw = *reinterpret_cast<const uint4*>(orow + col);
+        float acc[V::N], o[V::N];
+        V::unpack(hraw, acc);
+        V::unpack(oraw, o);
+#pragma unroll
+        for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(wk, o[j]));
+        V::store(h + col, acc);
+#pragma unroll
+        for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[j]); ss += r * r; }
+      }
+      ss = warp_sum(ss);
+      rmsnorm_row<T>(c, h, x, ss, lane);
+      if (lane == 0) {
+        tlayer[slot] = layer;
+        tpass[slot] = pass;
+        atomicAdd(&s_legs, 1ull);
+        if (home != c.rank) atomicAdd(&s_remote, 1ull);
+        s_home[lt] = retire ? -2 - home : home;  // counted on the home after the chunk's scatter
+      }
+      if (retire) {
+        if (lane == 0)
+          reinterpret_cast<unsigned long long*>(c.peer[home] + c.lay.tok_time)[2 * (uint64_t)slot + 1] = globaltimer_ns();
+        continue;
+      }
+      if (GATE && gw) {
+        gate_logits<T>(c, x, gw, gb, lane, zv);
+      } else if (!c.router) {
+        if (lane == 0) raise_fault(c, F_NO_ROUTER, slot, layer, pass);
+        continue;
+      }
+      int my_e;
+      float my_w;
+      route_select(zv, c.E, c.K, lane, my_e, my_w);
+      if (lane < c.K) {
+        reinterpret_cast<int32_t*>(c.peer[home] + c.lay.tok_idx)[(uint64_t)slot * c.K + lane] = my_e;
+        reinterpret_cast<float*>(c.peer[home] + c.lay.tok_w)[(uint64_t)slot * c.K + lane] = my_w;
+      }
+      if (lane == 0) {
+        PendingLeg p;
+        if (my_e < 0 || my_e >= c.E) {
+          raise_fault(c, F_EXPERT_RANGE, slot, my_e, layer);
+          p.r = -1;
+        } else {
+          p.r = c.owner[my_e];
+          p.q = layer * c.H + c.lq[my_e];
+        }
+        p.g.token_slot = slot; p.g.k = 0; p.g.home = (int16_t)home; p.g.w = my_w; p.g.seq = 0;
+        my[0] = p;
+      }
+    }
+    __syncthreads();
+    scatter_legs(c, legs, kTPC * c.KS);
+    __syncthreads();
+    // merged (and retired) counts on each token's home, once its state and next leg are
+    // visible: the home's amoe_run reads them for quiescence, as it reads the combine's
+    if (threadIdx.x < kTPC && s_home[threadIdx.x] != -1) {
+      const int v = s_home[threadIdx.x];
+      const int home = v >= 0 ? v : -2 - v;
+      unsigned long long* hst = reinterpret_cast<unsigned long long*>(c.peer[home] + c.lay.stats);
+      fence_sc(sys);
+      if (sys) {
+        atomicAdd_system(hst + 0, 1ull);
+        if (v < 0) atomicAdd_system(hst + 1, 1ull);
+      } else {
+        atomicAdd(hst + 0, 1ull);
+        if (v < 0) atomicAdd(hst + 1, 1ull);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long* st = wsp<unsigned long long>(c, c.rank, c.lay.stats);
+    if (s_legs) atomicAdd(st + 2, s_legs);
+    if (s_remote) atomicAdd(st + 3, s_remote);
+  }
+}
+
+int launch_direct_merge(const DevCtx& c, const GroupDev& g, int retire_pass, int num_sms, cudaStream_t s) {
+  const int grid = num_sms * 4;
+  if (c.dtype == AMOE_BF16) {
+    if (c.gate_on) launch_pdl(direct_merge_kernel<__nv_bfloat16, true>, dim3(grid), dim3(kTokThreads), 0, s, c, g, retire_pass);
+    else launch_pdl(direct_merge_kernel<__nv_bfloat16, false>, dim3(grid), dim3(kTokThreads), 0, s, c, g, retire_pass);
+  } else {
+    if (c.gate_on) launch_pdl(direct_merge_kernel<float, true>, dim3(grid), dim3(kTokThreads), 0, s, c, g, retire_pass);
+    else launch_pdl(direct_merge_kernel<float, false>, dim3(grid), dim3(kTokThreads), 0, s, c, g, retire_pass);
+  }
+  return 1;
+}
+
 // done[base + rank] = value on every rank (base 0: quiescence epoch; base AMOE_MAX_G: the
 // AMOE_SYNC layer-barrier sequence). Release: the stores of this rank's earlier kernels are
 // visible to a peer that observes the flag.
