@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--router", default="table", choices=["table", "gate"],
                     help="table: synthetic Zipf logits (the paper's eval); gate: device router gate "
                          "x·Wgᵀ + per-layer Zipf log-prob bias computed in the combine (SURVEY.md f3)")
+    ap.add_argument("--shift-every", type=int, default=1000,
+                    help="skew epoch length in layer-steps (BASELINE.json configs[3]: 1000; reading c6): the "
+                         "per-layer expert permutation is redrawn every that many layer traversals of the wave")
     ap.add_argument("--topk", type=int, default=0, help="override top-K (1: the paper's Top-1 routing, P:L463)")
     ap.add_argument("--direct", action="store_true",
                     help="top-1 direct forwarding (amoe_set_direct; needs --topk 1): the executing rank "
@@ -63,13 +66,14 @@ def FFN_KERNEL(d):
     return "ffn_tc_kernel<GATEUP> (tcgen05 UMMA 128x256, fused SwiGLU)"
 
 
-def config_dict(spec, L, T, G, policy, grouped, skew="zipf", router="table", direct=False):
+def config_dict(spec, L, T, G, policy, grouped, skew="zipf", router="table", direct=False, shift_every=1000):
     """The workload description shared by both arms' JSON lines."""
     return {"workload": f"{spec.name}-shaped expert layers: L={L} E={spec.E} top-{spec.K} S={spec.S} d={spec.d} "
                         f"ff={spec.ff}, {T} tokens in flight per GPU, "
                         + (f"Zipf s={spec.zipf_s}" if skew == "zipf" else "exponential λ=0.38") + " routing",
             "experts_per_gpu": f"e mod {G}", "policy": policy, "grouped": grouped, "router": router,
             "l2": "inputs larger than L2 (resident weights >> 126 MB); no flush",
+            "skew_shift_every_layer_steps": shift_every,
             "step": "one decode pass: every token through all L layers",
             "merge": "direct top-1 forwarding on the executing rank" if direct else "token pool + combine on the home"}
 
@@ -343,10 +347,15 @@ def main():
             w2 = torch.empty(d, ff, dtype=torch.bfloat16, device=dev).normal_(0, ff ** -0.5, generator=gen)
             ctx.set_expert(l, e, w1, w3, w2)
             wts.append((w1, w3, w2))
-    n_tab = 2
+    # router tables: one per pass when the skew epoch shifts within the run (every pass then
+    # carries its own epoch's permutations), else two alternating passes of epoch 0
+    n_pass = args.warmup + args.steps
+    shifting = args.shift_every < n_pass * L
+    n_tab = n_pass if shifting else 2
     tables_host = [wl.router_logits(args.seed, L, T, E, zipf_s=spec.zipf_s, pass_idx=p, token_offset=rank * T,
-                                    skew=args.skew)
+                                    skew=args.skew, shift_every=args.shift_every)
                    for p in range(n_tab)]
+    epochs = sorted({wl.skew_epoch(p, l, L, args.shift_every) for p in range(args.warmup, n_pass) for l in range(L)})
     table = torch.from_numpy(np.stack(tables_host)).to(dev).contiguous()
     ctx.set_router(table)
     if args.direct:
@@ -391,6 +400,7 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     launches0 = ctx.launch_count()
+    remote0 = int(ctx.state()["stats"][3])
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     runs = []
@@ -401,6 +411,7 @@ def main():
     barrier()
     clk = clocks.stop()
     launches = ctx.launch_count() - launches0
+    remote_legs = int(ctx.state()["stats"][3]) - remote0     # legs this rank ran for another home
     ms = ev0.elapsed_time(ev1)
     prof = ctx.profile_read()
     execs = ctx.exec_log()
@@ -461,11 +472,40 @@ def main():
                  "mean_legs_per_execution_rank0": round(my_legs / max(1, len(execs)), 1),
                  "legs_per_execution_hist_rank0": {f">={k}": v for k, v in sorted(hist.items())}}
 
+    # NVLink term: a leg run on a rank other than its token's home moves the
+    # x row home -> owner (the gather's peer load, d·2 B) and the output row owner -> home (the
+    # down epilogue's peer store, d·2 B) plus its 16-B ring entry; per rank and direction the
+    # larger of the two, against 900 GB/s; combined with the step roofline two ways (overlap:
+    # max, BASELINE.json's literal "plus": sum). Analytic need for uniform placement: 2·K·d·2·(G−1)/G
+    # bytes per homed token-layer (both directions).
+    per_rank_nv = D.gather_values([remote_legs, my_legs], device=cdev)
+    rem_max = max(v[0] for v in per_rank_nv)
+    nv_dir_bytes = rem_max * (d * 2 + 16) / args.steps             # per step, per direction, busiest rank
+    nv_peak = 900.0
+    t_nv_ms = nv_dir_bytes / (nv_peak * 1e9) * 1e3 * args.steps
+    legs_all = [v[1] for v in per_rank_nv]
+    share = max(legs_all) / max(1, sum(legs_all))
+    nvlink = {"bytes_per_step_per_direction_busiest_rank": int(nv_dir_bytes),
+              "gbs_per_direction": round(nv_dir_bytes / (step_ms / 1e3) / 1e9, 2), "peak": nv_peak, "unit": "GB/s",
+              "frac": round(nv_dir_bytes / (step_ms / 1e3) / 1e9 / nv_peak, 5),
+              "remote_legs_per_rank": [int(v[0]) for v in per_rank_nv],
+              "measured_bytes_per_token_layer": round(2 * sum(v[0] for v in per_rank_nv) * (d * 2 + 16)
+                                                      / max(1, G * T * L * args.steps), 1),
+              "analytic_bytes_per_token_layer_uniform": round(2 * K * d * 2 * (G - 1) / G, 1),
+              "t_nvlink_ms": round(t_nv_ms, 3),
+              "step_roofline_max_ms": round(max(t_roof_ms, t_nv_ms), 3),
+              "step_roofline_sum_ms": round(t_roof_ms + t_nv_ms, 3),
+              "frac_of_step_roofline_max": round(max(t_roof_ms, t_nv_ms) / ms, 4),
+              "frac_of_step_roofline_sum": round((t_roof_ms + t_nv_ms) / ms, 4)}
+    placement = {"legs_per_rank": [int(x) for x in legs_all], "hottest_rank_share": round(share, 4),
+                 "cap_speedup_vs_1gpu": round(1.0 / share, 3) if share else None,
+                 "note": "speedup over one GPU is bounded by 1 / the hottest rank's share of the legs (SURVEY.md §8(e))"}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
-        "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router, args.direct),
+        "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router, args.direct, args.shift_every),
         "gpu_launches": int(launches),
         "die_map_sms": list(amoe.die_info()),
         "clocks": clk,
@@ -484,7 +524,10 @@ def main():
                      "stage_ms_total": stage_ms,
                      "stage_launches": {k: v[1] for k, v in prof.items()},
                      "hbm_kernels": hbm,
-                     "step": step_roof},
+                     "step": step_roof,
+                     "nvlink": nvlink},
+        "placement": placement,
+        "skew_epochs_in_timed_region": epochs,
     }
 
     # ------------------------------------------------------------------ end to end (host buffers)

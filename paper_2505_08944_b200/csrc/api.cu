@@ -49,6 +49,7 @@ struct MapCacheEntry {
 struct amoe_ctx {
   amoe_config cfg;
   bool direct = false;                // top-1 direct forwarding (amoe_set_direct)
+  uint64_t merged_seen = 0;           // home merge counter at the end of the last amoe_run
   DevCtx dc;
   Layout lay;
   char* ws;
@@ -908,7 +909,10 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   if (st != AMOE_OK) return st;
   log_executions(c, true);
   const uint64_t* s0 = reinterpret_cast<const uint64_t*>(reinterpret_cast<const char*>(c->pinned) + c->lay.stats);
-  const uint64_t retired0 = s0[1], merged0 = s0[0], legs0 = s0[2];
+  // merged0: with direct forwarding at G > 1 a peer may already merge this home's tokens before
+  // this rank's first snapshot, so the baseline is where the previous run left the counter
+  const uint64_t retired0 = s0[1], legs0 = s0[2];
+  const uint64_t merged0 = (c->direct && c->cfg.G > 1) ? c->merged_seen : s0[0];
   bool announced = false;
   int idle_streak = 0;
   // AMOE_SYNC: the layer this rank may run, and whether it has arrived at that layer's barrier
@@ -1024,6 +1028,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       bool all = true;
       for (int r = 0; r < c->cfg.G; ++r) all &= done[r] == epoch;
       if (all) {
+        c->merged_seen = sv[0];
         rs.token_layers = (int64_t)(sv[0] - merged0);
         rs.legs = (int64_t)(sv[2] - legs0);
         break;

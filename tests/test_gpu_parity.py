@@ -358,7 +358,16 @@ def test_loopback_peers_match_single_gpu(G, monkeypatch):
     torch.cuda.synchronize()
     assert np.array_equal(h, to_np(c1.state()["h"]))
     remote = sum(int(c.state()["stats"][3]) for c in ctxs)
-    assert remote > 0
+    # the legs that crossed ranks (each moves its x row home -> owner and its output row back over
+    # the peer link: 2·d·2 bytes) are exactly the oracle's routed legs whose expert is owned by
+    # another rank than the token's home (owner e mod G)
+    expected = 0
+    for p in range(2):
+        for l in range(P.L):
+            for r in range(G):
+                idx, _ = nx.route_topk(P.tables[r][p % P.n_tab, l], P.K)
+                expected += int((idx % G != r).sum())
+    assert remote == expected > 0
 
 
 def test_box_depths_sum_every_rank(monkeypatch):

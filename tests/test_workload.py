@@ -53,3 +53,20 @@ def test_hottest_expert_share_matches_survey():
         idx = np.argsort(-z, axis=1, kind="stable")[:, :K]
         got = np.bincount(idx.ravel(), minlength=E).max() / idx.size
         assert abs(got - share) < 0.006, (E, K, got)
+
+
+def test_skew_shift_redraws_layer_permutations():
+    """Skew shifting (BASELINE.json configs[3], reading c6): with a 32-layer wave and an epoch of
+    32 layer-steps, pass 0 and pass 1 fall in different epochs, so every layer's expert
+    permutation is redrawn (the hot expert moves for most layers), while passes in the same epoch
+    share it. Checked on the generated logits, not only on skew_epoch."""
+    L, T, E = 32, 4000, 8
+    z0 = wl.router_logits(3, L, T, E, pass_idx=0, shift_every=32)
+    z1 = wl.router_logits(3, L, T, E, pass_idx=1, shift_every=32)
+    z0b = wl.router_logits(3, L, T, E, pass_idx=0, shift_every=1000)
+    z1b = wl.router_logits(3, L, T, E, pass_idx=1, shift_every=1000)
+    hot = lambda z: np.bincount(z.argmax(axis=1), minlength=E).argmax()
+    moved = sum(hot(z0[l]) != hot(z1[l]) for l in range(L))
+    same = sum(hot(z0b[l]) != hot(z1b[l]) for l in range(L))
+    assert moved >= L // 2          # a fresh permutation per layer: the hottest expert moves (7/8 chance)
+    assert same == 0                # one epoch: same permutation, only the Gumbel noise differs
