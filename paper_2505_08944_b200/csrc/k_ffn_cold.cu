@@ -281,6 +281,23 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
         const uint32_t full = smem_u32(&bars[s]);
         tma_load_3d(sb, &tmAct, 0, q * n_pad, KB * k, full);
       };
+      // the weight tensor maps live in the workspace (global memory): prefetch the ones this CTA's
+      // items use into the descriptor cache before the first loads
+      if (n_items > 0) {
+        int ph, t, k;
+        it.get(0, ph, t, k);
+        int q0 = ph == 0 ? t / a.ft : t / a.dt;
+        it.get(n_items - 1, ph, t, k);
+        int q1 = ph == 0 ? t / a.ft : t / a.dt;
+        if (it.a1 > it.a0 && it.b1 > it.b0) { q0 = 0; q1 = a.nq - 1; }
+        for (int q = q0; q <= q1 && q < q0 + 8; ++q) {
+          const CUtensorMap* cm = a.cmaps + a.qid[q] * 4;
+          if (KA == 1) { tma_prefetch(a.wmaps + a.qid[q] * 3); tma_prefetch(a.wmaps + a.qid[q] * 3 + 1); }
+          else { tma_prefetch(cm); tma_prefetch(cm + 1); }
+          tma_prefetch(cm + (KB == 2 ? 2 : 3));
+        }
+        tma_prefetch(&tmAct);
+      }
       // weights of the first stages stream before the grid dependency (they are constant)
       int stage = 0;
       uint32_t phase = 0;
