@@ -94,6 +94,8 @@ struct GroupDev {
   int32_t nq;
   int32_t rows_cap;
   int32_t max_tokens;
+  int32_t exact;                 // 1: drain exactly cap[q] legs per queue (the scheduler's count)
+  int32_t cap[AMOE_MAX_GROUP];
   int32_t* qinfo;          // [3*AMOE_MAX_GROUP]: n, row_off, start
   amoe_leg* meta;
   void* tile;

@@ -50,6 +50,9 @@ struct amoe_ctx {
   amoe_config cfg;
   bool direct = false;                // top-1 direct forwarding (amoe_set_direct)
   uint64_t merged_seen = 0;           // home merge counter at the end of the last amoe_run
+  const int32_t* exact_caps = nullptr;  // set by amoe_run's pipelined loop around a pick's launches
+  uint32_t* snapbuf[3] = {nullptr, nullptr, nullptr};   // pipelined loop: rotating pinned snapshots
+  cudaEvent_t snapev[3] = {nullptr, nullptr, nullptr};
   DevCtx dc;
   Layout lay;
   char* ws;
@@ -554,6 +557,10 @@ static amoe_status make_group(amoe_ctx* c, const amoe_group* g, int max_tokens, 
   gd->rows_cap = g->rows_cap;
   gd->max_tokens = max_tokens > 0 ? max_tokens : 0;
   if (c->cfg.max_batch > 0 && (gd->max_tokens == 0 || gd->max_tokens > c->cfg.max_batch)) gd->max_tokens = c->cfg.max_batch;
+  if (c->exact_caps) {   // amoe_run's pipelined loop: the drain count is the scheduler's
+    gd->exact = 1;
+    for (int q = 0; q < g->nq; ++q) gd->cap[q] = c->exact_caps[q];
+  }
   gd->qinfo = g->qinfo;
   gd->meta = g->meta;
   gd->tile = g->tile;
@@ -868,6 +875,12 @@ static int32_t group_rows(const amoe_ctx* c, const amoe_group& g, int j, const u
   return (int32_t)Q[(size_t)g.layer[j] * H + lq];
 }
 
+// local queue index (l*H + lq) of the group's j-th queue
+static int group_qidx(const amoe_ctx* c, const amoe_group& g, int j, int H) {
+  const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
+  return g.layer[j] * H + lq;
+}
+
 // consumer head (snapshot) of the group's j-th queue
 static uint32_t group_head(const amoe_ctx* c, const amoe_group& g, int j, int H) {
   const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
@@ -974,12 +987,94 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   // AMOE_DEFRAG_GLOBAL at G > 1: every poll first reads the box-wide per-block depths from all
   // ranks' queue counters (peer_depths_kernel -> gtot, inside the snapshot range)
   const bool global_look = p->policy == AMOE_DEFRAG_GLOBAL && c->cfg.G > 1;
-  for (;;) {
+  // Pipelined picks (asynchronous policies, closed loop): the host decides pick k + 1 while pick k
+  // runs, instead of waiting for the stream after every pick. Queue depths come from the newest
+  // counter snapshot that has landed (copied asynchronously behind each pick) minus what the
+  // host itself has drained since — every drain takes exactly the count the host decided
+  // (GroupDev::exact / the cold kernel's n), so the host's consumer heads are exact and its depth
+  // estimate never exceeds the published count. At most two picks are in flight; stale views only
+  // delay decisions (idleness and quiescence are judged on a fresh view). AMOE_PIPELINE=0 off.
+  const char* pl_env = getenv("AMOE_PIPELINE");
+  const bool pipe = !sync && !stepping && grow_ns == 0 && !combine_first && !split_pick &&
+                    !(pl_env && pl_env[0] == '0');
+  const int NQ = L * H;
+  std::vector<uint32_t> head_host, commit_seen;
+  struct Outst { int buf; };
+  std::vector<Outst> outst;        // FIFO of snapshots in flight (oldest first)
+  int view_buf = -1;               // snapshot buffer the loop reads (pipelined)
+  bool dirty = false, want_fresh = false;
+  uint64_t launches_at_view = 0;   // c->launches when the current view's copy was issued
+  uint64_t combine_launch_mark = 0;  // c->launches right after the last combine was issued
+  if (pipe) {
+    for (int i = 0; i < 3; ++i) {
+      if (!c->snapbuf[i] && cudaMallocHost(&c->snapbuf[i], c->snap_bytes) != cudaSuccess) return AMOE_ECUDA;
+      if (!c->snapev[i] && cudaEventCreateWithFlags(&c->snapev[i], cudaEventDisableTiming) != cudaSuccess)
+        return AMOE_ECUDA;
+    }
+    memcpy(c->snapbuf[0], c->pinned, c->snap_bytes);
+    view_buf = 0;
+    const uint32_t* qs = c->pinned + c->lay.qctr / 4;
+    head_host.resize(NQ);
+    commit_seen.resize(NQ);
+    for (int i = 0; i < NQ; ++i) { head_host[i] = qs[4 * i + 2]; commit_seen[i] = qs[4 * i + 1]; }
+    launches_at_view = c->launches;
+  }
+  auto issue_snapshot = [&]() -> amoe_status {
+    // a free buffer: not the view, not in flight
+    int b = 0;
+    for (; b < 3; ++b) {
+      bool busy = b == view_buf;
+      for (const auto& o : outst) busy |= o.buf == b;
+      if (!busy) break;
+    }
     if (global_look) c->launches += launch_peer_depths(c->dc, s);
-    st = snapshot(c, s);   // waits for this rank's previous launches: the GPU is idle from here
-    if (st != AMOE_OK) return st;
+    CK(cudaMemcpyAsync(c->snapbuf[b], c->ws, c->snap_bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->snapev[b], s));
+    outst.push_back({b});
+    return AMOE_OK;
+  };
+  std::vector<uint64_t> outst_launches;   // c->launches when each in-flight copy was issued
+  uint64_t issued_mark = c->launches;     // c->launches when the newest copy was issued
+  auto consume = [&](bool all) -> amoe_status {
+    while (!outst.empty()) {
+      const int b = outst.front().buf;
+      if (all || outst.size() >= 2) {
+        CK(cudaEventSynchronize(c->snapev[b]));
+      } else {
+        const cudaError_t q = cudaEventQuery(c->snapev[b]);
+        if (q == cudaErrorNotReady) break;
+        if (q != cudaSuccess) return AMOE_ECUDA;
+      }
+      view_buf = b;
+      launches_at_view = outst_launches.front();
+      outst.erase(outst.begin());
+      outst_launches.erase(outst_launches.begin());
+      const uint32_t* qs = c->snapbuf[b] + c->lay.qctr / 4;
+      for (int i = 0; i < NQ; ++i)
+        if ((int32_t)(qs[4 * i + 1] - commit_seen[i]) > 0) commit_seen[i] = qs[4 * i + 1];
+    }
+    return AMOE_OK;
+  };
+  for (;;) {
+    if (pipe) {
+      dirty = dirty || (uint64_t)c->launches != issued_mark;
+      if (dirty) {
+        if ((st = issue_snapshot()) != AMOE_OK) return st;
+        issued_mark = c->launches;
+        outst_launches.push_back(c->launches);
+        dirty = false;
+      }
+      if ((st = consume(want_fresh)) != AMOE_OK) return st;
+      want_fresh = false;
+    } else {
+      if (global_look) c->launches += launch_peer_depths(c->dc, s);
+      st = snapshot(c, s);   // waits for this rank's previous launches: the GPU is idle from here
+      if (st != AMOE_OK) return st;
+    }
+    // fresh: the view reflects every launch this rank issued
+    const bool fresh = !pipe || (outst.empty() && !dirty && launches_at_view == (uint64_t)c->launches);
     const auto t_poll = clk::now();
-    const char* snap = reinterpret_cast<const char*>(c->pinned);
+    const char* snap = pipe ? reinterpret_cast<const char*>(c->snapbuf[view_buf]) : reinterpret_cast<const char*>(c->pinned);
     if (*reinterpret_cast<const uint32_t*>(snap + c->lay.err)) return abort_run(0, 0, 0, 0);
     if (c->cfg.G > 1) {
       const uint32_t* dn = reinterpret_cast<const uint32_t*>(snap + c->lay.done);
@@ -992,7 +1087,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       }
     }
     const uint64_t* sv = reinterpret_cast<const uint64_t*>(snap + c->lay.stats);
-    log_executions(c, false);
+    if (!pipe) log_executions(c, false);   // pipelined: executions are logged as they are issued
     if (sync && !announced && !stepping) {
       const uint32_t* flags = reinterpret_cast<const uint32_t*>(snap + c->lay.done) + AMOE_MAX_G;
       if (!sync_arrived && (int64_t)(sv[0] - merged0) >= expected * (int64_t)(rs.barriers + 1) &&
@@ -1034,12 +1129,16 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         break;
       }
     }
-    depths_from_snapshot(c, Q.data());
+    if (pipe)
+      for (int i = 0; i < NQ; ++i) Q[i] = commit_seen[i] - head_host[i];
+    else
+      depths_from_snapshot(c, Q.data());
     if (sync)   // lockstep: only the current layer's queues are eligible
       for (int bb = 0; bb < L; ++bb)
         if (bb != sync_layer) std::fill(Q.begin() + (size_t)bb * H, Q.begin() + (size_t)(bb + 1) * H, 0u);
     const uint32_t* cc = reinterpret_cast<const uint32_t*>(snap + c->lay.cctr);
-    const uint32_t cpend = cc[1] - cc[2];
+    // pending merges; a view taken before the last combine launch no longer tells
+    const uint32_t cpend = (pipe && combine_launch_mark > launches_at_view) ? 0u : cc[1] - cc[2];
     if (combine_first && cpend > 0) {
       // merge the tokens whose last legs arrived from other ranks before picking: their next
       // layer's legs join the queues first, so the pick drains one batch instead of a fragment
@@ -1111,10 +1210,12 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         int cap = group_rows(c, g, j, Q.data(), H);
         if (c->cfg.max_batch > 0) cap = std::min(cap, c->cfg.max_batch);
         cold_caps[j] = cap;
-        cold_start[j] = group_head(c, g, j, H);
+        cold_start[j] = pipe ? head_host[group_qidx(c, g, j, H)] : group_head(c, g, j, H);
         cold_max = std::max(cold_max, cap);
       }
       const bool cold_pick = cold_pick_ok(c, cold_max, g.nq);
+      // pipelined: every drain of this pick takes exactly the host's count (cold_caps)
+      if (pipe) c->exact_caps = cold_caps;
       if (split_pick && n_cold > 0 && n_cold < g.nq) {
         amoe_group gc = g, gh = g;
         gc.nq = gh.nq = 0;
@@ -1152,15 +1253,28 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         if ((st = amoe_rebatch_ffn_forward(c, &g, 0, s)) != AMOE_OK) return st;
         rs.picks += 1;
       }
+      c->exact_caps = nullptr;
+      if (pipe)
+        for (int j = 0; j < g.nq; ++j) {
+          const int qi = group_qidx(c, g, j, H);
+          head_host[qi] += (uint32_t)cold_caps[j];
+          if (c->prof && cold_caps[j] > 0) { c->exec_log.push_back(qi); c->exec_log.push_back(cold_caps[j]); }
+        }
       if (!c->direct && (st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
+      combine_launch_mark = c->launches;
       rs.kernel_launches += c->launches - l0;
       rs.queues_run += g.nq;
       idle_streak = 0;
     } else if (cpend > 0) {
       const int64_t l0 = c->launches;
       if ((st = amoe_combine(c, retire_pass, s)) != AMOE_OK) return st;
+      combine_launch_mark = c->launches;
       rs.kernel_launches += c->launches - l0;
       idle_streak = 0;
+    } else if (!fresh) {
+      // nothing decidable on a stale view: wait for the newest snapshot (the in-flight picks'
+      // merges may have queued the next layer) before judging idleness
+      want_fresh = true;
     } else {
       rs.idle_polls += 1;
       if (stepping) {
@@ -1190,6 +1304,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       }
       if (++idle_streak > 64) std::this_thread::sleep_for(std::chrono::microseconds(5));
       rs.idle_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t_poll).count();
+      if (pipe) { dirty = true; want_fresh = true; }   // poll: a new snapshot next time round
     }
     if (stepping && rs.picks >= p->max_picks) {
       rs.token_layers = (int64_t)(sv[0] - merged0);   // merges observed up to this pick's launch
@@ -1274,6 +1389,10 @@ amoe_status amoe_destroy(amoe_ctx_t c) {
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
+  for (int i = 0; i < 3; ++i) {
+    if (c->snapbuf[i]) cudaFreeHost(c->snapbuf[i]);
+    if (c->snapev[i]) cudaEventDestroy(c->snapev[i]);
+  }
   delete c;
   return AMOE_OK;
 }

@@ -81,7 +81,13 @@ __global__ void __launch_bounds__(kDrainThreads) drain_kernel(DevCtx c, GroupDev
     head[q] = ctr[2];
     rv[q] = r;
     if (r - head[q] > c.ring_cap) raise_fault(c, F_RING_OVERFLOW, g.qid[q], r, head[q]);
-    if (cm == r) {
+    if (g.exact) {
+      // the scheduler's count (<= the published count it saw): taken whole. When no producer is
+      // mid-flight (commit == reserve) the acquire on commit already covers every entry below it;
+      // otherwise the entries of [head, head + cap) are waited for below
+      avail[q] = (uint32_t)g.cap[q];
+      if (!(cm == r && avail[q] <= cm - head[q])) slow[atomicAdd(&nslow, 1)] = q;
+    } else if (cm == r) {
       avail[q] = cm - head[q];
     } else {
       avail[q] = 0;
@@ -89,6 +95,23 @@ __global__ void __launch_bounds__(kDrainThreads) drain_kernel(DevCtx c, GroupDev
     }
   }
   __syncthreads();
+  if (g.exact) {
+    for (int sq = 0; sq < nslow; ++sq) {
+      const int q = slow[sq];
+      const amoe_leg* ring = ring_ptr(c, c.rank, g.qid[q]);
+      for (uint32_t i = tid; i < avail[q]; i += blockDim.x) {
+        const uint32_t pos = head[q] + i;
+        if (ld_acquire(&ring[pos & c.ring_mask].seq) != pos + 1u) {
+          const uint64_t t0 = globaltimer_ns();
+          while (ld_acquire(&ring[pos & c.ring_mask].seq) != pos + 1u)
+            if (globaltimer_ns() - t0 > 4000000000ull) { raise_fault(c, F_STALE_ENTRY, g.qid[q], pos, 0); break; }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) nslow = 0;
+    __syncthreads();
+  }
   // slow path: a producer on a peer is mid-flight; the published prefix is where seq == pos+1
   for (int s = 0; s < nslow; ++s) {
     const int q = slow[s];
