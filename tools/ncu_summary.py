@@ -30,21 +30,31 @@ def launches(path):
     hdr, data = rows[hi], rows[hi + 1:]
     ki, mi, vi, ui = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     agg = collections.OrderedDict()
+    dram = collections.defaultdict(float)
     unit = None
     for r in data:
-        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        if r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[ui], 1)
+            dram[name] += float(r[vi].replace(",", "")) * f
+            continue
+        if r[mi] != "gpu__time_duration.sum":
             continue
         unit = r[ui]
-        name = r[ki].split("(")[0].replace("void ", "")
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += float(r[vi].replace(",", ""))
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}.get(unit, 1e-6)
-    hot = {k: v for k, v in agg.items() if "amoe" in k or "ffn_" in k}
+    torch_like = ("distribution", "Fill", "elementwise", "arange", "die_probe", "spin_kernel", "reduce_kernel<")
+    hot = {k: v for k, v in agg.items() if not any(t in k for t in torch_like) or "splitk" in k}
     tot = sum(v[1] for v in hot.values())
-    print(f"| kernel | launches | total ms | mean us | share of libamoe time |\n|---|---|---|---|---|")
+    print(f"| kernel | launches | total ms | mean us | share of libamoe time | DRAM MB per launch | DRAM GB/s |\n|---|---|---|---|---|---|---|")
     for k, (n, t) in sorted(hot.items(), key=lambda x: -x[1][1]):
-        print(f"| `{k}` | {n} | {t * scale:.2f} | {1e3 * t * scale / n:.1f} | {100 * t / tot:.2f}% |")
+        mb = dram.get(k, 0.0) / n / 1e6
+        gbs = dram.get(k, 0.0) / (t * scale * 1e-3) / 1e9 if t else 0.0
+        print(f"| `{k}` | {n} | {t * scale:.2f} | {1e3 * t * scale / n:.1f} | {100 * t / tot:.2f}% | {mb:.1f} | {gbs:.0f} |")
     other = {k: v for k, v in agg.items() if k not in hot}
     if other:
         print("\nNon-libamoe kernels in the same process (setup: weight init, arange):")
