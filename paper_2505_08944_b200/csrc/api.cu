@@ -881,6 +881,8 @@ static int group_qidx(const amoe_ctx* c, const amoe_group& g, int j, int H) {
   return g.layer[j] * H + lq;
 }
 
+constexpr int kSmallQueue = 16;   // legs: a queue this small is pure weight streaming (§5.4)
+
 // consumer head (snapshot) of the group's j-th queue
 static uint32_t group_head(const amoe_ctx* c, const amoe_group& g, int j, int H) {
   const int lq = g.expert[j] >= c->cfg.E ? c->Hr + (g.expert[j] - c->cfg.E) : c->dc.lq[g.expert[j]];
@@ -953,6 +955,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   // opt-in: measured slower at every T tried (the second drain + gather + FFN launches cost more
   // than the cold queues gain on the 1-CTA kernels, profiles/r01_T_sweep.md)
   const bool split_pick = c->cfg.dtype == AMOE_BF16 && sp_env && sp_env[0] == '1';
+  // opt-in (AMOE_MIXED_SPLIT=1): a pick mixing small and hot queues runs the small ones in the
+  // fused cold kernel and the rest on the tensor-core path; measured neutral to -4 % on the
+  // DeepSeek waves (T = 512: 1.27 -> 1.22 M; larger T never mixes, profiles/r02/mixed_split_ab.md)
+  const char* ms_env = getenv("AMOE_MIXED_SPLIT");
+  const bool mixed_split = !split_pick && !c->direct && ms_env && ms_env[0] == '1';
   int sync_layer = c->start_layer;
   bool sync_arrived = false;
   // barrier flag value: (run epoch, barrier index + 1), so ranks agree without shared history
@@ -1214,6 +1221,8 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
         cold_max = std::max(cold_max, cap);
       }
       const bool cold_pick = cold_pick_ok(c, cold_max, g.nq);
+      int n_small = 0;
+      for (int j = 0; j < g.nq; ++j) n_small += cold_caps[j] <= kSmallQueue;
       // pipelined: every drain of this pick takes exactly the host's count (cold_caps)
       if (pipe) c->exact_caps = cold_caps;
       if (split_pick && n_cold > 0 && n_cold < g.nq) {
@@ -1243,6 +1252,29 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
           c->launches += launch_direct_merge(c->dc, gd, retire_pass, c->num_sms, s);
         }
         CK(cudaGetLastError());
+        rs.picks += 1;
+      } else if (!cold_pick && mixed_split && c->cfg.dtype == AMOE_BF16 && n_small >= 2 && n_small < g.nq) {
+        // a pick mixing small queues (<= 16 legs: pure weight streaming) with hot ones: the small
+        // queues run in one fused cold launch, the hot ones on the tensor-core path behind it
+        amoe_group gc = g, gh = g;
+        gc.nq = gh.nq = 0;
+        int cc_caps[AMOE_MAX_GROUP], ch_caps[AMOE_MAX_GROUP];
+        uint32_t cc_start[AMOE_MAX_GROUP];
+        for (int j = 0; j < g.nq; ++j) {
+          const bool small = cold_caps[j] <= kSmallQueue;
+          amoe_group& t = small ? gc : gh;
+          t.layer[t.nq] = g.layer[j];
+          t.expert[t.nq] = g.expert[j];
+          if (small) { cc_caps[gc.nq] = cold_caps[j]; cc_start[gc.nq] = cold_start[j]; }
+          else ch_caps[gh.nq] = cold_caps[j];
+          ++t.nq;
+        }
+        gh.max_rows_hint = 1 << 30;   // the hot part stays on the tensor-core path
+        c->exact_caps = nullptr;
+        if ((st = cold_ffn_forward(c, &gc, cc_caps, cc_start, s)) != AMOE_OK) return st;
+        if (pipe) c->exact_caps = ch_caps;
+        if ((st = amoe_rebatch(c, &gh, 0, s)) != AMOE_OK) return st;
+        if ((st = expert_ffn(c, &gh, 1, s)) != AMOE_OK) return st;
         rs.picks += 1;
       } else if (cold_pick) {
         // every queue of the pick is cold: the fused one-launch path, each queue drained up to
