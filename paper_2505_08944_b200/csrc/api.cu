@@ -52,7 +52,8 @@ struct amoe_ctx {
   uint64_t merged_seen = 0;           // home merge counter at the end of the last amoe_run
   const int32_t* exact_caps = nullptr;  // set by amoe_run's pipelined loop around a pick's launches
   uint32_t* snapbuf[3] = {nullptr, nullptr, nullptr};   // pipelined loop: rotating pinned snapshots
-  cudaEvent_t snapev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t snapev[6] = {};          // [b]: copy b landed; [3 + b]: compute stream reached copy b
+  cudaStream_t copy_stream = nullptr;  // the snapshot copies' side stream
   DevCtx dc;
   Layout lay;
   char* ws;
@@ -967,6 +968,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   using clk = std::chrono::steady_clock;
   const auto t_run0 = clk::now();
   auto finish = [&](amoe_run_stats* out) {
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);   // no snapshot copy outlives the run
     rs.wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(clk::now() - t_run0).count();
     if (out) *out = rs;
   };
@@ -1013,11 +1015,13 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   uint64_t launches_at_view = 0;   // c->launches when the current view's copy was issued
   uint64_t combine_launch_mark = 0;  // c->launches right after the last combine was issued
   if (pipe) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 3; ++i)
       if (!c->snapbuf[i] && cudaMallocHost(&c->snapbuf[i], c->snap_bytes) != cudaSuccess) return AMOE_ECUDA;
+    for (int i = 0; i < 6; ++i)
       if (!c->snapev[i] && cudaEventCreateWithFlags(&c->snapev[i], cudaEventDisableTiming) != cudaSuccess)
         return AMOE_ECUDA;
-    }
+    if (!c->copy_stream && cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return AMOE_ECUDA;
     memcpy(c->snapbuf[0], c->pinned, c->snap_bytes);
     view_buf = 0;
     const uint32_t* qs = c->pinned + c->lay.qctr / 4;
@@ -1035,8 +1039,15 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       if (!busy) break;
     }
     if (global_look) c->launches += launch_peer_depths(c->dc, s);
-    CK(cudaMemcpyAsync(c->snapbuf[b], c->ws, c->snap_bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(c->snapev[b], s));
+    // the copy runs on a side stream behind an event: the compute stream goes straight from this
+    // pick's merge to the next pick's kernels, so programmatic dependent launch overlaps their
+    // prologues (a copy between them on the same stream would serialise every boundary). The
+    // copy may also see later picks' counter updates: every field the loop reads is monotone or
+    // re-checked (published counts, merge / retire counts, flags)
+    CK(cudaEventRecord(c->snapev[3 + b], s));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->snapev[3 + b], 0));
+    CK(cudaMemcpyAsync(c->snapbuf[b], c->ws, c->snap_bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+    CK(cudaEventRecord(c->snapev[b], c->copy_stream));
     outst.push_back({b});
     return AMOE_OK;
   };
@@ -1421,10 +1432,11 @@ amoe_status amoe_destroy(amoe_ctx_t c) {
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 3; ++i)
     if (c->snapbuf[i]) cudaFreeHost(c->snapbuf[i]);
+  for (int i = 0; i < 6; ++i)
     if (c->snapev[i]) cudaEventDestroy(c->snapev[i]);
-  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
   return AMOE_OK;
 }
