@@ -952,15 +952,11 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   std::vector<uint64_t> prev_depth(grow_ns > 0 ? c->cfg.L : 0, 0);
   int grow_layer = -1;
   auto grow_t0 = std::chrono::steady_clock::now();
-  const char* sp_env = getenv("AMOE_SPLIT_PICK");
-  // opt-in: measured slower at every T tried (the second drain + gather + FFN launches cost more
-  // than the cold queues gain on the 1-CTA kernels, profiles/r01_T_sweep.md)
-  const bool split_pick = c->cfg.dtype == AMOE_BF16 && sp_env && sp_env[0] == '1';
   // opt-in (AMOE_MIXED_SPLIT=1): a pick mixing small and hot queues runs the small ones in the
   // fused cold kernel and the rest on the tensor-core path; measured neutral to -4 % on the
   // DeepSeek waves (T = 512: 1.27 -> 1.22 M; larger T never mixes, profiles/r02/mixed_split_ab.md)
   const char* ms_env = getenv("AMOE_MIXED_SPLIT");
-  const bool mixed_split = !split_pick && !c->direct && ms_env && ms_env[0] == '1';
+  const bool mixed_split = !c->direct && ms_env && ms_env[0] == '1';
   int sync_layer = c->start_layer;
   bool sync_arrived = false;
   // barrier flag value: (run epoch, barrier index + 1), so ranks agree without shared history
@@ -1004,7 +1000,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   // estimate never exceeds the published count. At most two picks are in flight; stale views only
   // delay decisions (idleness and quiescence are judged on a fresh view). AMOE_PIPELINE=0 off.
   const char* pl_env = getenv("AMOE_PIPELINE");
-  const bool pipe = !sync && !stepping && grow_ns == 0 && !combine_first && !split_pick &&
+  const bool pipe = !sync && !stepping && grow_ns == 0 && !combine_first &&
                     !(pl_env && pl_env[0] == '0');
   const int NQ = L * H;
   std::vector<uint32_t> head_host, commit_seen;
@@ -1213,12 +1209,6 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       g.max_rows_hint = 0;
       for (int j = 0; j < g.nq; ++j) g.max_rows_hint = std::max(g.max_rows_hint, group_rows(c, g, j, Q.data(), H));
       const int64_t l0 = c->launches;
-      // AMOE_SPLIT_PICK=1: a pick that mixes cold queues (<= 128 rows: weight-streaming) with hot
-      // ones runs as two launches on the same stream, cold first: the cold part gets the 1-CTA / split-K kernels
-      // instead of padding 256-row pair tiles (profiles/r01_T_sweep.md). Buffers are reused:
-      // the second drain is stream-ordered behind the first group's forward.
-      int n_cold = 0;
-      for (int j = 0; j < g.nq; ++j) n_cold += group_rows(c, g, j, Q.data(), H) <= 128;
       // cold pick: every queue drains <= 128 legs (its snapshot depth, or the max_batch cap),
       // from its consumer head in the snapshot
       int cold_caps[AMOE_MAX_GROUP];
@@ -1236,22 +1226,7 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
       for (int j = 0; j < g.nq; ++j) n_small += cold_caps[j] <= kSmallQueue;
       // pipelined: every drain of this pick takes exactly the host's count (cold_caps)
       if (pipe) c->exact_caps = cold_caps;
-      if (split_pick && n_cold > 0 && n_cold < g.nq) {
-        amoe_group gc = g, gh = g;
-        gc.nq = gh.nq = 0;
-        gc.max_rows_hint = gh.max_rows_hint = 0;
-        for (int j = 0; j < g.nq; ++j) {
-          const int32_t r = group_rows(c, g, j, Q.data(), H);
-          amoe_group& t = r <= 128 ? gc : gh;
-          t.layer[t.nq] = g.layer[j];
-          t.expert[t.nq] = g.expert[j];
-          t.max_rows_hint = std::max(t.max_rows_hint, r);
-          ++t.nq;
-        }
-        if ((st = amoe_rebatch_ffn_forward(c, &gc, 0, s)) != AMOE_OK) return st;
-        if ((st = amoe_rebatch_ffn_forward(c, &gh, 0, s)) != AMOE_OK) return st;
-        rs.picks += 1;   // one pick, two launches
-      } else if (c->direct) {
+      if (c->direct) {
         // top-1 direct forwarding (f3): drain + gather, SwiGLU expert into the group's out rows,
         // then this rank merges, normalises, routes and scatters each token itself
         if ((st = amoe_rebatch(c, &g, 0, s)) != AMOE_OK) return st;
