@@ -182,3 +182,30 @@ def test_execute_cold_explicit_drain_and_head_check():
     with pytest.raises(AmoeError) as ei:
         ctx.check()
     assert ei.value.info[:4] == [12, 0, 119, 120]
+
+
+def test_execute_cold_ragged_with_empty_queue_and_maximum():
+    """One fused cold launch over three DeepSeek-shaped queues holding 0, 5 and the 128-leg
+    maximum: the empty queue drains nothing and stores nothing, the others match the oracle row
+    for row, and the heads advance by exactly the drained counts."""
+    from paper_2505_08944_b200 import amoe
+    E, T = 3, 133
+    P = Problem(L=1, E=E, K=1, S=0, d=2048, ff=1408, T=T, seed=19, n_tab=1)
+    ctx = P.make_ctx()
+    slots = torch.arange(T, dtype=torch.int32, device="cuda")
+    ctx.token_init(slots, dev_tensor(P.h0[0], "bf16"), 0)
+    idx = np.array([1] * 5 + [2] * 128, dtype=np.int32).reshape(T, 1)
+    ctx.enqueue(0, slots, topk_idx=torch.from_numpy(idx).cuda(), topk_w=torch.ones(T, 1, device="cuda"))
+    gb = amoe.GroupBuffers(ctx, 3 * 128 + 256).set_queues([(0, 0), (0, 1), (0, 2)])
+    ctx.execute_cold(gb, [0, 0, 0], [0, 5, 128])
+    torch.cuda.synchronize()
+    ctx.check()
+    n, _, start = gb.info()
+    assert n.tolist() == [0, 5, 128] and start.tolist() == [0, 0, 0]
+    assert ctx.queue_depths()[0].tolist()[:3] == [0, 0, 0]
+    st = ctx.state()
+    assert int(st["stats"][2]) == 133
+    x0, pool = to_np(st["x"]), to_np(st["pool"])[:, 0]
+    for e, rows in ((1, np.arange(5)), (2, np.arange(5, T))):
+        ref = nx.expert_ffn(x0[rows], *P.W[(0, e)])
+        assert floored_err(pool[rows], ref) <= TOL["bf16"], e
