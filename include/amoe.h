@@ -294,7 +294,7 @@ amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t ctx, const amoe_group* grp, int 
  * n[q] <= its published depth (the scheduler's decision) — gathers their x rows,
  * runs the SwiGLU expert and stores every output row into its home's token pool (a7). Writes
  * grp->qinfo (n, row offset, start); uses grp->act ([nq * n_pad, ff], n_pad = max n rounded up
- * to 16). bf16 contexts only (EINVAL otherwise). A head that is not start[q] latches device fault
+ * to 16). bf16 contexts with d % 256 == 0 only (EINVAL otherwise). A head that is not start[q] latches device fault
  * 12 (queue, start, head); an entry never published traps after 4 s (ECUDA). */
 amoe_status amoe_execute_cold(amoe_ctx_t ctx, const amoe_group* grp, const uint32_t* start, const int32_t* n,
                               void* stream);

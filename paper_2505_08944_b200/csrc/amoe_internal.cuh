@@ -61,7 +61,7 @@ struct Layout {
   uint64_t tok_idx;    // i32[T][K]
   uint64_t tok_time;   // u64[T][2]: globaltimer (ns) at admission (token_init) and at retirement
   uint64_t wmaps;      // CUtensorMap[L*H][3]
-  uint64_t cmaps;      // CUtensorMap[L*H][4]: K-block views (3-D) W1 x2, W3 x2, W2 x2, W2 x4 (cold kernel)
+  uint64_t cmaps;      // CUtensorMap[L*H][4]: K-block views (3-D) W1 x2, W3 x2, W2 x2, W2 x1 (cold kernel)
   uint64_t wptrs;      // u64[L*H][3]
   uint64_t gate;       // u64[L][2]: router gate weights [E][d] (storage dtype) and bias [E] fp32, or 0
   uint64_t s_tile, s_meta, s_qinfo, s_act, s_out;   // amoe_run's group scratch

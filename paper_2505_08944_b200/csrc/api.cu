@@ -396,14 +396,14 @@ amoe_status amoe_set_expert(amoe_ctx_t c, int layer, int expert, const void* w1,
         !encode_bf16_2d(&maps[2], w2, c->cfg.d, c->cfg.ff, 128))
       return AMOE_ECUDA;
     CK(cudaMemcpy(c->ws + c->lay.wmaps + (uint64_t)slot * 3 * 128, maps, sizeof(maps), cudaMemcpyHostToDevice));
-    // K-block views for the cold kernel: W1 / W3 two K blocks deep, W2 two and four (a view
-    // whose depth does not divide the K extent stays zero and is never selected)
+    // K-block views for the cold kernel: W1 / W3 two K blocks deep (128 rows), W2 two and one
+    // deep over 256-row tiles (a view whose depth does not divide K stays zero, never selected)
     CUtensorMap cm[4];
     memset(cm, 0, sizeof(cm));
     encode_bf16_kb3d(&cm[0], w1, c->cfg.ff, c->cfg.d, 128, 2);
     encode_bf16_kb3d(&cm[1], w3, c->cfg.ff, c->cfg.d, 128, 2);
-    encode_bf16_kb3d(&cm[2], w2, c->cfg.d, c->cfg.ff, 128, 2);
-    encode_bf16_kb3d(&cm[3], w2, c->cfg.d, c->cfg.ff, 128, 4);
+    encode_bf16_kb3d(&cm[2], w2, c->cfg.d, c->cfg.ff, 256, 2);   // down: 256-row tiles (§5.4)
+    encode_bf16_kb3d(&cm[3], w2, c->cfg.d, c->cfg.ff, 256, 1);
     CK(cudaMemcpy(c->ws + c->lay.cmaps + (uint64_t)slot * 4 * 128, cm, sizeof(cm), cudaMemcpyHostToDevice));
   }
   for (int i = 0; i < 3; ++i) c->wptrs[(size_t)slot * 3 + i] = ptrs[i];
@@ -665,19 +665,17 @@ amoe_status amoe_expert_ffn_forward(amoe_ctx_t c, const amoe_group* g, void* str
 // The fused cold path (k_ffn_cold.cu) vs the four-kernel path for a pick whose queues hold at
 // most n_max legs each (nq queues): AMOE_COLD=1 forces the fused kernel (n_max <= 128), 0 the
 // four-kernel path; by default the fused kernel takes the picks where it measured faster
-// (profiles/r02_cold_sweep.md, device time per pick on one B200):
+// (profiles/r02/cold_sweep_v3.log, device time per pick on one B200):
 //  * n_max <= 16: every shape (weight streaming dominates; one launch, no grid-wide hand-off);
-//  * n_max <= 32: unless the pick streams more than 1 GB of weights (Mixtral-sized groups);
-//  * n_max <= 64: DeepSeek-sized experts (d <= 2048) in groups of >= 4.
+//  * n_max <= 32: Mixtral-sized experts (d >= 4096) or groups of >= 4 experts.
+// d % 256 == 0 (the fused kernel's down tiles are 256 rows).
 static bool cold_pick_ok(const amoe_ctx* c, int n_max, int nq) {
-  if (c->cfg.dtype != AMOE_BF16 || n_max < 1 || n_max > 128) return false;
+  if (c->cfg.dtype != AMOE_BF16 || n_max < 1 || n_max > 128 || c->cfg.d % 256) return false;
   const char* e = getenv("AMOE_COLD");
   if (e && e[0] == '1') return true;
   if (e && e[0] == '0') return false;
-  const double wbytes = 6.0 * c->cfg.d * c->cfg.ff * nq;
   if (n_max <= 16) return true;
-  if (n_max <= 32) return wbytes <= 1e9;
-  if (n_max <= 64) return c->cfg.d <= 2048 && nq >= 4;
+  if (n_max <= 32) return c->cfg.d >= 4096 || nq >= 4;
   return false;
 }
 
@@ -691,7 +689,7 @@ static amoe_status cold_ffn_forward(amoe_ctx* c, const amoe_group* g, const int*
   int wslot[AMOE_MAX_GROUP];
   amoe_status st = make_group(c, g, 0, &gd, wslot);
   if (st != AMOE_OK) return st;
-  if (c->cfg.dtype != AMOE_BF16 || !g->act || !n || !start) return AMOE_EINVAL;
+  if (c->cfg.dtype != AMOE_BF16 || !g->act || !n || !start || c->cfg.d % 256) return AMOE_EINVAL;
   int nmax = 1;
   for (int q = 0; q < g->nq; ++q) {
     if (n[q] < 0 || n[q] > 128) return AMOE_EINVAL;

@@ -52,9 +52,9 @@ constexpr int kPartFloats = NMAX * 256;   // one partial slot: [leg][256] fp32 (
 
 struct ColdArgs {
   int32_t nq, n_pad, stages, stage_bytes;
-  int32_t ka, kb;             // K blocks (64 wide) per iteration: gate/up (1, 2), down (2, 4)
+  int32_t ka, kb;             // K blocks (64 wide) per iteration: gate/up (1, 2), down (1, 2)
   int32_t ipt_a, ipt_b;       // iterations per tile: d/(64·ka) (gate/up), ff/(64·kb) (down)
-  int32_t ft, dt;             // tiles per queue: ff/128 (gate/up), d/128 (down)
+  int32_t ft, dt;             // tiles per queue: ff/128 (gate/up), d/256 (down: two 128-row halves)
   int32_t ia, ib;             // iterations per phase (all queues)
   int32_t pa, pb;             // CTAs streaming each phase (<= grid)
   int32_t ctr_a, ctr_b, ctr_act;
@@ -63,7 +63,7 @@ struct ColdArgs {
   int32_t* qinfo;             // out [3*AMOE_MAX_GROUP]: drained n, row offset, ring start per queue
   __nv_bfloat16* act;         // [nq*n_pad][ff]: SwiGLU activations
   const CUtensorMap* wmaps;   // [L*H][3]: 2-D maps (box 64 x 128)
-  const CUtensorMap* cmaps;   // [L*H][4]: K-block views W1 x2, W3 x2, W2 x2, W2 x4
+  const CUtensorMap* cmaps;   // [L*H][4]: K-block views W1 x2, W3 x2 (128 rows), W2 x2, W2 x1 (256 rows)
   int32_t qid[AMOE_MAX_GROUP];     // l*H + lq
   int32_t n[AMOE_MAX_GROUP];       // legs to drain (<= NMAX; the scheduler's snapshot depth)
   uint32_t start[AMOE_MAX_GROUP];  // ring position of the first (= the queue's consumer head)
@@ -246,7 +246,7 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
         const uint32_t sa = smem_u32(ring + s * stage_bytes);
         const uint32_t full = smem_u32(&bars[s]);
         // stage: gate/up: W1 [KA][128][64], W3 [KA][128][64], legs [KA][n_pad][64];
-        //        down:    W2 [KB][128][64], act [KB][n_pad][64]
+        //        down:    W2 [KB][256][64] (two 128-row halves per K block), act [KB][n_pad][64]
         if (ph == 0) {
           mbar_expect_tx(full, 2 * KA * A_BYTES);
           const int q = t / a.ft, f = t - q * a.ft;
@@ -260,11 +260,11 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
             tma_load_3d_hint(sa + KA * A_BYTES, cm + 1, 0, f * 128, KA * k, full, wpol);
           }
         } else {
-          mbar_expect_tx(full, KB * (A_BYTES + n_pad * 128));
+          mbar_expect_tx(full, KB * (2 * A_BYTES + n_pad * 128));
           mbar_arrive_cnt(full, 64);                  // the gather lanes' share (no gather here)
           const int q = t / a.dt, dtl = t - q * a.dt;
           const CUtensorMap* cm = a.cmaps + a.qid[q] * 4 + (KB == 2 ? 2 : 3);
-          tma_load_3d_hint(sa, cm, 0, dtl * 128, KB * k, full, wpol);
+          tma_load_3d_hint(sa, cm, 0, dtl * 256, KB * k, full, wpol);
         }
       };
       int ready_q = -1;                               // queue whose activations are all stored
@@ -277,7 +277,7 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
           proxy_fence_global();
           ready_q = q;
         }
-        const uint32_t sb = smem_u32(ring + s * stage_bytes) + KB * A_BYTES;
+        const uint32_t sb = smem_u32(ring + s * stage_bytes) + KB * 2 * A_BYTES;
         const uint32_t full = smem_u32(&bars[s]);
         tma_load_3d(sb, &tmAct, 0, q * n_pad, KB * k, full);
       };
@@ -401,11 +401,15 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
 #endif
         {
           for (int kb = 0; kb < KB; ++kb) {
-            const uint64_t a0d = umma_desc_sw128(sa + kb * A_BYTES);
-            const uint64_t b0d = umma_desc_sw128(sa + KB * A_BYTES + kb * n_pad * 128);
+            // rows 0..127 and 128..255 of the 256-row W2 slab into the two accumulator halves
+            const uint64_t a0d = umma_desc_sw128(sa + kb * 2 * A_BYTES), a1d = umma_desc_sw128(sa + kb * 2 * A_BYTES + A_BYTES);
+            const uint64_t b0d = umma_desc_sw128(sa + KB * 2 * A_BYTES + kb * n_pad * 128);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(d0, a0d + 2 * kk, b0d + 2 * kk, idesc, (!first || kb > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t accum = (!first || kb > 0 || kk > 0) ? 1u : 0u;
+              umma_bf16(d0, a0d + 2 * kk, b0d + 2 * kk, idesc, accum);
+              umma_bf16(d0 + (uint32_t)n_pad, a1d + 2 * kk, b0d + 2 * kk, idesc, accum);
+            }
           }
         }
         umma_commit(smem_u32(&bars[MAXS + stage]));
@@ -560,7 +564,7 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
     auto count_legs = [&](int q, int tl) {
       if (et < a.n[q]) {
         const amoe_leg& e = s_leg[et];
-        leg_pieces_done(dc, e.home, e.token_slot, e.k, 128u);
+        leg_pieces_done(dc, e.home, e.token_slot, e.k, 256u);
       }
       if (tl == 0) {
         const uint32_t rem = __popc(__ballot_sync(0xffffffffu, et < a.n[q] && s_leg[et].home != dc.rank));
@@ -597,28 +601,30 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
         float* part = a.part + (size_t)((ph * 2 + which) * MAXP + cta) * kPartFloats;
         for (int c0 = 0; c0 < n; c0 += 16) {
           float v[32];
-          if (ph == 0) tmem_ld16x2(tb + c0, tb + n_pad + c0, v);     // v[0..16) gate, v[16..32) up
-          else tmem_ld16(tb + c0, v);
+          // v[0..16): gate (gate/up) or output rows 0..127 (down); v[16..32): up, or rows 128..255
+          tmem_ld16x2(tb + c0, tb + n_pad + c0, v);
           const int m = min(16, n - c0);
           if (whole) {
             // thread r holds column r of 16 leg rows: transpose through smem, then every row
-            // (256 B: the tile's 128 columns) leaves as 16-B vector stores
-            for (int i = 0; i < m; ++i)
-              s_stage[i][r] = __float2bfloat16_rn(ph == 0 ? silu_mul(v[i], v[16 + i]) : v[i]);
-            epi_bar();
-            for (int x = et; x < m * 16; x += 128) {
-              const int tk = x >> 4, cc = x & 15;
-              const uint4 val = reinterpret_cast<const uint4*>(s_stage[tk])[cc];
-              __nv_bfloat16* dst = ph == 0 ? a.act + (uint64_t)(q * n_pad + c0 + tk) * dc.ff + tl * 128
-                                           : dst_row(c0 + tk) + tl * 128;
-              reinterpret_cast<uint4*>(dst)[cc] = val;
+            // (256 B: 128 columns) leaves as 16-B vector stores; down tiles store two halves
+            for (int half = 0; half < (ph == 0 ? 1 : 2); ++half) {
+              for (int i = 0; i < m; ++i)
+                s_stage[i][r] = __float2bfloat16_rn(ph == 0 ? silu_mul(v[i], v[16 + i]) : v[16 * half + i]);
+              epi_bar();
+              for (int x = et; x < m * 16; x += 128) {
+                const int tk = x >> 4, cc = x & 15;
+                const uint4 val = reinterpret_cast<const uint4*>(s_stage[tk])[cc];
+                __nv_bfloat16* dst = ph == 0 ? a.act + (uint64_t)(q * n_pad + c0 + tk) * dc.ff + tl * 128
+                                             : dst_row(c0 + tk) + tl * 256 + half * 128;
+                reinterpret_cast<uint4*>(dst)[cc] = val;
+              }
+              epi_bar();
             }
-            epi_bar();
           } else {
             for (int i = 0; i < m; ++i) {
               float* row = part + (size_t)(c0 + i) * 256;
               row[r] = v[i];
-              if (ph == 0) row[128 + r] = v[16 + i];
+              row[128 + r] = v[16 + i];
             }
           }
         }
@@ -658,21 +664,21 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
                     const float* slot = a.part + (size_t)((ph * 2 + which_of(ob + i2, t, pt)) * MAXP + ob + i2) * kPartFloats;
                     const float* r0 = slot + (size_t)tk0 * 256 + 4 * ch0;
                     pg0[i2] = __ldcg(reinterpret_cast<const float4*>(r0));
-                    if (ph == 0) pu0[i2] = __ldcg(reinterpret_cast<const float4*>(r0 + 128));
+                    pu0[i2] = __ldcg(reinterpret_cast<const float4*>(r0 + 128));
                     if (ok1) {
                       const float* r1 = slot + (size_t)tk1 * 256 + 4 * ch1;
                       pg1[i2] = __ldcg(reinterpret_cast<const float4*>(r1));
-                      if (ph == 0) pu1[i2] = __ldcg(reinterpret_cast<const float4*>(r1 + 128));
+                      pu1[i2] = __ldcg(reinterpret_cast<const float4*>(r1 + 128));
                     }
                   }
 #pragma unroll
                 for (int i2 = 0; i2 < 4; ++i2)
                   if (ob + i2 <= lastc) {
                     g0.x += pg0[i2].x; g0.y += pg0[i2].y; g0.z += pg0[i2].z; g0.w += pg0[i2].w;
-                    if (ph == 0) { u0.x += pu0[i2].x; u0.y += pu0[i2].y; u0.z += pu0[i2].z; u0.w += pu0[i2].w; }
+                    u0.x += pu0[i2].x; u0.y += pu0[i2].y; u0.z += pu0[i2].z; u0.w += pu0[i2].w;
                     if (ok1) {
                       g1.x += pg1[i2].x; g1.y += pg1[i2].y; g1.z += pg1[i2].z; g1.w += pg1[i2].w;
-                      if (ph == 0) { u1.x += pu1[i2].x; u1.y += pu1[i2].y; u1.z += pu1[i2].z; u1.w += pu1[i2].w; }
+                      u1.x += pu1[i2].x; u1.y += pu1[i2].y; u1.z += pu1[i2].z; u1.w += pu1[i2].w;
                     }
                   }
               }
@@ -688,9 +694,13 @@ ffn_cold_kernel(const __grid_constant__ CUtensorMap tmAct, const __grid_constant
                   *reinterpret_cast<uint2*>(a.act + (uint64_t)(q * n_pad + tok) * dc.ff + tl * 128 + 4 * ch) =
                       *reinterpret_cast<uint2*>(o2);
                 } else {
+                  __nv_bfloat16* drow = dst_row(tok) + tl * 256 + 4 * ch;
                   o2[0] = __floats2bfloat162_rn(g.x, g.y);
                   o2[1] = __floats2bfloat162_rn(g.z, g.w);
-                  *reinterpret_cast<uint2*>(dst_row(tok) + tl * 128 + 4 * ch) = *reinterpret_cast<uint2*>(o2);
+                  *reinterpret_cast<uint2*>(drow) = *reinterpret_cast<uint2*>(o2);
+                  o2[0] = __floats2bfloat162_rn(u.x, u.y);
+                  o2[1] = __floats2bfloat162_rn(u.z, u.w);
+                  *reinterpret_cast<uint2*>(drow + 128) = *reinterpret_cast<uint2*>(o2);
                 }
               }
             }
@@ -748,23 +758,23 @@ void cold_blocks(int d, int ff, int n_pad, int* ka, int* kb) {
   using namespace cold;
   if (const char* e = getenv("AMOE_COLD_KAKB")) {   // A/B override "ka,kb" (profiles/r02_cold_sweep.md)
     int x = 0, y = 0;
-    if (sscanf(e, "%d,%d", &x, &y) == 2 && (x == 1 || x == 2) && (y == 2 || y == 4) && (d / 64) % x == 0 &&
+    if (sscanf(e, "%d,%d", &x, &y) == 2 && (x == 1 || x == 2) && (y == 1 || y == 2) && (d / 64) % x == 0 &&
         (ff / 64) % y == 0) {
       *ka = x;
       *kb = y;
       return;
     }
   }
-  const int cand[3][2] = {{2, 4}, {2, 2}, {1, 2}};
+  const int cand[4][2] = {{2, 2}, {1, 2}, {2, 1}, {1, 1}};
   for (const auto& ck : cand) {
-    const int sb = std::max(ck[0] * (2 * A_BYTES + n_pad * 128), ck[1] * (A_BYTES + n_pad * 128));
+    const int sb = std::max(ck[0] * (2 * A_BYTES + n_pad * 128), ck[1] * (2 * A_BYTES + n_pad * 128));
     if ((d / 64) % ck[0] || (ff / 64) % ck[1] || RING_BUDGET / sb < 3) continue;
     *ka = ck[0];
     *kb = ck[1];
     return;
   }
   *ka = 1;
-  *kb = 2;
+  *kb = 1;
 }
 
 int launch_ffn_cold(const DevCtx& c, int nq, const int* qid, const int* n, const uint32_t* start, int n_pad, int ka,
@@ -784,13 +794,13 @@ int launch_ffn_cold(const DevCtx& c, int nq, const int* qid, const int* n, const
   a.n_pad = n_pad;
   a.ka = ka;
   a.kb = kb;
-  a.stage_bytes = std::max(ka * (2 * A_BYTES + n_pad * 128), kb * (A_BYTES + n_pad * 128));
+  a.stage_bytes = std::max(ka * (2 * A_BYTES + n_pad * 128), kb * (2 * A_BYTES + n_pad * 128));
   a.stages = std::min(MAXS, RING_BUDGET / a.stage_bytes);
   if (a.stages < 2) return -1;
   a.ipt_a = c.d / (64 * ka);
   a.ipt_b = c.ff / (64 * kb);
   a.ft = c.ff / 128;
-  a.dt = c.d / 128;
+  a.dt = c.d / 256;
   const int tiles_a = nq * a.ft, tiles_b = nq * a.dt;
   a.ia = tiles_a * a.ipt_a;
   a.ib = tiles_b * a.ipt_b;
@@ -816,6 +826,10 @@ int launch_ffn_cold(const DevCtx& c, int nq, const int* qid, const int* n, const
   }
   const int cap_sms = std::min(num_sms, MAXP);
   auto plan = [&](int tiles, int ipt, int width) {
+    // long tiles (>= 32 iterations: Mixtral's gate/up and down) make every segment a large
+    // stream of weights next to which a partial is small: split freely over every SM. Short
+    // tiles (DeepSeek) bound the split by the partial bytes the last arriver reads
+    if (ipt >= 32) return std::min(cap_sms, tiles * ipt);
     const int64_t part_bytes = (int64_t)n_pad * width * 4;
     const int max_seg = (int)std::max<int64_t>(1, ((int64_t)red_kb << 10) / part_bytes);
     // nseg <= ceil(ipt·P/I) + 1, so P <= tiles·(max_seg - 1) keeps every tile within max_seg
@@ -824,7 +838,7 @@ int launch_ffn_cold(const DevCtx& c, int nq, const int* qid, const int* n, const
     return (int)std::min<int64_t>({(int64_t)cap_sms, (int64_t)tiles * ipt, p});
   };
   a.pa = plan(tiles_a, a.ipt_a, 256);
-  a.pb = plan(tiles_b, a.ipt_b, 128);
+  a.pb = plan(tiles_b, a.ipt_b, 256);
   const int P = std::max(a.pa, a.pb);
   launch_pdl(ffn_cold_kernel, dim3(P), dim3(THREADS), SMEM_DYN, s, tm_act, a, c);
   return 1;

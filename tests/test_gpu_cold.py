@@ -73,7 +73,7 @@ def _run(P, idx, w, cold, hint):
 
 @pytest.mark.parametrize("d,ff,E,K,T", [
     (512, 1024, 8, 2, 300),        # 75 legs per expert
-    (128, 256, 8, 2, 68),          # tiny widths, 17 legs per expert (grid limited to the work)
+    (256, 256, 8, 2, 68),          # small widths, 17 legs per expert (grid limited to the work)
     (2048, 1408, 8, 1, 1024),      # DeepSeek-shaped, 8 experts at the 128-leg maximum
     (2048, 1408, 1, 1, 1),         # one DeepSeek expert, one token
     (2048, 1408, 64, 6, 512),      # 64 DeepSeek experts in one launch, 48 legs each
