@@ -466,6 +466,58 @@ def test_loopback_amoe_run_concurrent_ranks(G, d, policy, sms, monkeypatch):
     assert np.array_equal(h, to_np(c1.state()["h"]))
 
 
+@pytest.mark.parametrize("G,policy", [(2, "defrag"), (8, "defrag"), (4, "defrag_global")])
+def test_loopback_pipelined_loop_concurrent_ranks(G, policy, monkeypatch):
+    """The pipelined scheduler loop at G > 1 (asynchronous snapshot copies on a side stream,
+    host-exact consumer heads, exact-count drains while peers' legs keep arriving): the default
+    at one routed expert per rank (G = 8 here), forced at G = 2 / 4 by turning the G > 1
+    merge-first / grow-wait heuristics off. Bit-identical to one rank."""
+    monkeypatch.setenv("AMOE_COLD", "0")
+    monkeypatch.setenv("AMOE_GROW_WAIT", "0")
+    monkeypatch.setenv("AMOE_COMBINE_FIRST", "0")
+    import threading
+    T = 64
+    P = Problem(L=3, E=8, K=2, S=0, d=128, ff=256, T=T, G=G, seed=17)
+    ctxs = [P.make_ctx(rank=r) for r in range(G)]
+    ptrs = [c.ws.data_ptr() for c in ctxs]
+    for c in ctxs:
+        c.import_peers(ptrs)
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    for r, c in enumerate(ctxs):
+        with torch.cuda.stream(streams[r]):
+            admit(c, P, rank=r)
+    torch.cuda.synchronize()
+    stats, errs = [None] * G, []
+
+    def worker(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                stats[r] = ctxs[r].run(retire_pass=2, policy=policy, stream=streams[r])
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append((r, e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "amoe_run did not terminate"
+    assert not errs, errs
+    torch.cuda.synchronize()
+    for c in ctxs:
+        c.check()
+    assert sum(s["token_layers"] for s in stats) == G * T * P.L * 2
+    h = np.concatenate([to_np(c.state()["h"]) for c in ctxs])
+    P1 = Problem(L=3, E=8, K=2, S=0, d=128, ff=256, T=G * T, G=1, seed=17)
+    P1.tables = [np.concatenate(P.tables, axis=2)]
+    P1.h0 = [np.concatenate(P.h0)]
+    c1 = P1.make_ctx()
+    admit(c1, P1)
+    c1.run(retire_pass=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(h, to_np(c1.state()["h"]))
+
+
 # ---------------------------------------------------------------- device faults
 
 def test_fault_expert_out_of_range_is_latched():
