@@ -442,8 +442,16 @@ def main():
     hbm_pk, hbm_kind = peak_hbm()
     my_tl = sum(r["token_layers"] for r in runs)
     hbm = {}
+    # AMOE_CP_GATHER=1 (one GPU, CTA-pair FFN): the re-batch gather runs inside the gate/up
+    # producer (cp.async copies of the legs' x rows); "rebatch" is then the drain
+    fused_gather = (G == 1 and os.environ.get("AMOE_CP_GATHER", "0") == "1" and d % 256 == 0
+                    and os.environ.get("AMOE_FFN_1CTA", "0") != "1" and not args.direct)
     for name, nbytes, ms_ in (("combine", my_tl * ((K + S) * d * 2 + 3 * d * 2 + E * 4), prof["combine"][0]),
                               ("rebatch", my_legs * 4 * d, prof["rebatch"][0])):
+        if name == "rebatch" and fused_gather:
+            hbm[name] = {"fused": "gather inside the gate/up GEMM's producer warp (cp.async A rows from x)",
+                         "drain_ms": round(ms_, 3), "gather_kernel_bytes": 0}
+            continue
         if ms_:
             gbs = nbytes / (ms_ / 1e3) / 1e9
             hbm[name] = {"achieved": round(gbs, 1), "peak": hbm_pk, "unit": "GB/s", "frac": round(gbs / hbm_pk, 3),

@@ -751,12 +751,25 @@ amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_
     }
     return cold_ffn_forward(c, g, n, start, s);
   }
-  // The fused gather is correct (tests) but slower on B200: each A row is re-read by every N tile
-  // of its raster group and TMA tile::gather4 moves ~6.6 B/cycle/SM vs >40 for tiled loads
-  // (profiles/r01_fused_gather.md), so the materialised gather (2·d bytes per leg, once) wins.
-  // Opt in with AMOE_FUSED_GATHER=1.
+  // The TMA tile::gather4 variant of the fused gather (AMOE_FUSED_GATHER=1) is correct (tests)
+  // but slow on B200: each A row is re-read by every N tile of its raster group and gather4
+  // moves ~6.6 B/cycle/SM vs >40 for tiled loads (profiles/r01_fused_gather.md).
+  // AMOE_CP_GATHER=1 (one GPU, bf16, CTA-pair kernel, hot picks): the gate/up producer warp
+  // copies the legs' x rows into its A stages with cp.async (16-B chunks, L2 hits after the first
+  // N tile) instead of a gather kernel materialising the tile (2·d·2 HBM bytes per leg); the GEMMs
+  // read the drained legs from the rings. Correct (bitwise equal to the materialised path) but
+  // slower on B200: the LSU gather holds the gate/up GEMM at ~0.68 of the tensor pipe against
+  // 0.97-0.98 with tiled TMA A loads (Mixtral 1.49 vs 1.84 M token-layers/s, DeepSeek 6.4 vs
+  // 7.3 M), so the materialised gather stays the default. Peer rows (G > 1)
+  // never take it: an A row is re-read by every N tile of its raster group.
   const char* fg = getenv("AMOE_FUSED_GATHER");
-  if (fg && fg[0] == '1' && c->cfg.G == 1 && c->cfg.dtype == AMOE_BF16) {
+  const char* cg = getenv("AMOE_CP_GATHER");
+  const char* e1 = getenv("AMOE_FFN_1CTA");
+  const bool cp_gather = (cg && cg[0] == '1') && !(fg && fg[0] == '1') && c->cfg.G == 1 &&
+                         c->cfg.dtype == AMOE_BF16 && c->cfg.d % 256 == 0 && c->num_sms >= 2 &&
+                         !(e1 && e1[0] == '1') && g && (g->max_rows_hint == 0 || g->max_rows_hint > 128) &&
+                         (uint64_t)c->cfg.T_slots * (uint64_t)c->cfg.d * 2u < (1ull << 32);
+  if (cp_gather || (fg && fg[0] == '1' && c->cfg.G == 1 && c->cfg.dtype == AMOE_BF16)) {
     // a4 drain only; the gather happens inside the gate/up GEMM's A-operand load
     GroupDev gd;
     amoe_status st = make_group(c, g, max_tokens, &gd, nullptr);
@@ -765,7 +778,7 @@ amoe_status amoe_rebatch_ffn_forward(amoe_ctx_t c, const amoe_group* g, int max_
       StageTimer tm(c, ST_REBATCH, s);
       c->launches += launch_drain(c->dc, gd, s);
     }
-    return expert_ffn(c, g, 1, s, 1);
+    return expert_ffn(c, g, 1, s, cp_gather ? 2 : 1);
   }
   amoe_status st = amoe_rebatch(c, g, max_tokens, s);
   if (st != AMOE_OK) return st;

@@ -51,7 +51,8 @@ struct FfnArgs {
   int32_t group_m;       // M tiles per raster group (L2 reuse of the weight slab)
   int32_t fuse;          // DOWN: 1 = store rows straight into the home token pools (fused a7)
   int32_t ring_legs;     // 1 = the drained legs are read from the µ-queue rings (no meta copy)
-  int32_t gather;        // GATEUP: 1 = A rows gathered from x by token slot (TMA tile::gather4)
+  int32_t gather;        // GATEUP: A rows gathered from x by token slot: 1 = TMA tile::gather4,
+                         // 2 = cp.async by the producer warp (CTA-pair kernel only)
   int32_t allow_split;   // split K when the output tiles cannot fill the machine (cold experts)
   int32_t atrim;         // partial M tiles load only their valid A rows
   int32_t die_sched;     // CTA-pair kernels: 0 static raster; dynamic claims through the unit
@@ -642,10 +643,12 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
   if (threadIdx.x == 0) FFN_TRACE(0, globaltimer_ns());
   __shared__ unsigned long long s_fwd[2];
   __shared__ int4 s_epi_rec[1];            // die schedule: the epilogue's current unit
+  __shared__ __align__(8) uint64_t s_afull[STAGES2];   // cp.async gather: A rows of a stage landed
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tiles = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2_BYTES);
+  const bool gcp = MODE == MODE_GATEUP && args.gather == 2;
   // bars: full[S], empty[S], tfull[2], tempty[2]   (full/tempty used in the leader only)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
   int* s_n = reinterpret_cast<int*>(tmem_holder + 4);
@@ -680,7 +683,13 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     for (int q = 0; q < nq; ++q) mn = max(mn, s_n[q]);
     s_start[AMOE_MAX_GROUP + 1] = mn;
     s_fwd[0] = 0; s_fwd[1] = 0;
-    for (int s = 0; s < STAGES2; ++s) { mbar_init(smem_u32(&bars[s]), 1); mbar_init(smem_u32(&bars[STAGES2 + s]), 1); }
+    // cp.async gather (gcp): a stage's full barrier also takes one arrival per CTA from its
+    // relay thread (A rows landed); each CTA's s_afull collects its producer lanes' cp.async
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(smem_u32(&bars[s]), gcp ? 3 : 1);   // (one relay arrival per CTA per stage)
+      mbar_init(smem_u32(&bars[STAGES2 + s]), 1);
+      if (gcp) mbar_init(smem_u32(&s_afull[s]), kWarp);
+    }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
       mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 2);     // one arrive per CTA of the pair
@@ -697,7 +706,9 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
         for (int q = 0; q < nq; ++q) { s_pre_d[d * (AMOE_MAX_GROUP + 1) + q] = a2; a2 += (s_n[q] + BM2 - 1) / BM2 * nbd; }
         s_pre_d[d * (AMOE_MAX_GROUP + 1) + nq] = a2;
       }
-      for (int r = 0; r < RING; ++r) { mbar_init(smem_u32(&ring_full[r]), 1); mbar_init(smem_u32(&ring_empty[r]), 4); }
+      // consumers of a published unit: leader MMA + epilogue, peer producer + epilogue (+ each
+      // CTA's relay thread under the cp.async gather)
+      for (int r = 0; r < RING; ++r) { mbar_init(smem_u32(&ring_full[r]), 1); mbar_init(smem_u32(&ring_empty[r]), gcp ? 6 : 4); }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&tmA);
@@ -831,7 +842,111 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
     return rec;
   };
 
-  if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
+  if (gcp && warp == 0) {
+    // ===================== producer with the re-batch gather fused (both CTAs, whole warp):
+    // this CTA's 128 A rows of a stage are the legs' x rows, copied by cp.async 16-B chunks
+    // straight from x[token_slot] into the 128-B-swizzled stage (lanes 8j..8j+7 write the 8
+    // chunks of one row: conflict-free), rows >= n zero-filled; the lanes' copies arrive on
+    // s_afull when they land (noinc), and the relay thread hands the stage to the leader. The B
+    // half is a TMA load onto the leader's full barrier, as in the tiled producer. The token
+    // slots of the next unit's rows are loaded while the current unit streams (no drain-to-GEMM
+    // bubble per unit). Every A row is re-read by each N tile of its raster group, from L2: the
+    // same L2 traffic as the materialised tile, without the gather kernel's HBM round trip
+    // (2·d·2 bytes per leg) — single GPU only (peer rows would cross NVLink once per N tile).
+    const char* xb = reinterpret_cast<const char*>(dc.peer[dc.rank] + dc.lay.x);
+    const uint32_t rowbytes = (uint32_t)dc.d * 2u;
+    const int rsub = lane >> 3, csub = lane & 7;
+    const amoe_leg* rings = reinterpret_cast<const amoe_leg*>(dc.peer[dc.rank] + dc.lay.rings);
+    auto bcast = [&](int4 u) -> int4 {
+      u.x = __shfl_sync(0xffffffffu, u.x, 0); u.y = __shfl_sync(0xffffffffu, u.y, 0);
+      u.z = __shfl_sync(0xffffffffu, u.z, 0); u.w = __shfl_sync(0xffffffffu, u.w, 0);
+      return u;
+    };
+    // token slot of rows lane + 32 j of this CTA's half of unit u's M tile (-1: row >= n)
+    auto slots_of = [&](int4 u, int (&sl)[4]) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int row = u.y * BM2 + (int)crank * 128 + lane + 32 * j;
+        sl[j] = -1;
+        if (u.x >= 0 && row < s_n[u.x])
+          sl[j] = rings[(uint64_t)(args.wslot[u.x] / 3) * dc.ring_cap +
+                        (((uint32_t)s_start[u.x] + (uint32_t)row) & dc.ring_mask)].token_slot;
+      }
+    };
+    int4 U = make_int4(-1, 0, 0, 0);
+    if (lane == 0) U = !die_sched ? static_unit(0) : leader ? claim_publish(0) : ring_get(0);
+    U = bcast(U);
+    int sl[4];
+    slots_of(U, sl);
+    int stage = 0; uint32_t phase = 0;
+    for (int it = 0; U.x >= 0; ++it) {
+      const int q = U.x, nb = U.z, ks = U.w;
+      const int kb0 = ks * kb_n / split, kb1 = (ks + 1) * kb_n / split;
+      const CUtensorMap* bmap = args.wmaps + args.wslot[q] + args.w_which + crank;
+      const int brow = nb * 128;
+      int4 Un = make_int4(-1, 0, 0, 0);
+      int sn[4] = {-1, -1, -1, -1};
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const uint32_t full_leader = mapa(smem_u32(&bars[stage]), 0);
+        const uint32_t sa = smem_u32(tiles + stage * STAGE2_BYTES);
+        if (lane == 0) {
+          mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1u);
+          if (leader) mbar_expect_tx(smem_u32(&bars[stage]), 2 * HALF_BYTES);   // the two B halves
+          tma_load_2d_pair(sa + HALF_BYTES, bmap, kb * BK, brow, full_leader);
+        }
+        __syncwarp();
+        // this lane's 32 chunks: 16-B chunk csub of rows 4u + rsub (whole 128-B lines per
+        // instruction); row r's slot lives in lane r % 32, register r / 32
+        const char* src = xb + (uint64_t)kb * (BK * 2) + csub * 16;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int row = 4 * u + rsub;
+          const int sv = __shfl_sync(0xffffffffu, sl[u >> 3], row & 31);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                       :: "r"(sa + (uint32_t)row * 128u + ((uint32_t)(csub ^ (row & 7)) << 4)),
+                          "l"(src + (sv < 0 ? 0u : (uint32_t)sv * rowbytes)), "r"(sv < 0 ? 0u : 16u) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(&s_afull[stage])) : "memory");
+        if (kb == kb0) {
+          // the next unit (the leader resolves and publishes it here, as the tiled producer
+          // does) and its rows' token slots, in flight while this unit streams
+          if (lane == 0) {
+            if (!die_sched) Un = static_unit(it + 1);
+            else if (leader) { advance(it); Un = next_unit; }
+            else Un = ring_get(it + 1);
+          }
+          Un = bcast(Un);
+          slots_of(Un, sn);
+        }
+        if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
+      }
+      U = Un;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sl[j] = sn[j];
+    }
+  } else if (gcp && warp == 3 && lane == 0) {
+    // ===================== relay (both CTAs): a stage's A rows landed (every producer lane's
+    // cp.async arrived on s_afull) -> order them for the tensor core (generic -> async proxy)
+    // and arrive on the leader's full barrier. Walks the same units as the producer.
+    // The arrive is RELAXED: a release at cluster scope compiles to MEMBAR.ALL.GPU, which cost
+    // ~1.5 us per stage here (ncu: the relay's membar stalls held the gate/up GEMM at 46 % of
+    // the tensor pipe). The copies are complete (observed through s_afull) and the proxy fence
+    // has made them visible to the async proxy before the arrive is issued.
+    int stage = 0; uint32_t phase = 0;
+    const uint32_t full0 = mapa(smem_u32(&bars[0]), 0);
+    for (int it = 0;; ++it) {
+      const int4 U = die_sched ? ring_get(it) : static_unit(it);
+      if (U.x < 0) break;
+      const int kb0 = U.w * kb_n / split, kb1 = (U.w + 1) * kb_n / split;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(smem_u32(&s_afull[stage]), phase);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
+                     :: "r"(full0 + (uint32_t)stage * 8u) : "memory");
+        if (++stage == STAGES2) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 0 && (lane == 0 || (MODE == MODE_GATEUP && args.gather))) {
     // ===================== TMA producer (both CTAs): own A half + own B half, bytes land on
     // the leader's full barrier (whole warp when A rows are gathered: lane i -> rows 4i..4i+3)
     int stage = 0; uint32_t phase = 0;
@@ -919,7 +1034,13 @@ ffn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const FfnArgs args, cons
 #ifdef AMOE_TRACE
         const unsigned long long tf0 = globaltimer_ns();
 #endif
-        mbar_wait(smem_u32(&bars[stage]), phase);
+        if (gcp) {
+          // A rows written by both CTAs' cp.async (generic proxy, fenced by the relays)
+          mbar_wait_cluster(smem_u32(&bars[stage]), phase);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        } else {
+          mbar_wait(smem_u32(&bars[stage]), phase);
+        }
 #ifdef AMOE_TRACE
         const unsigned long long tf1 = globaltimer_ns();
         t_wait_full += tf1 - tf0;
@@ -1333,7 +1454,7 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   a.sched = reinterpret_cast<uint32_t*>(c.peer[c.rank] + c.lay.sched);
     const char* et = getenv("AMOE_ATRIM");
   a.atrim = et ? (et[0] == '1') : 1;
-  a.ring_legs = gathered;
+  a.ring_legs = gathered ? 1 : 0;
   a.gather = (part == 1) ? gathered : 0;
   for (int q = 0; q < f.nq; ++q) a.wslot[q] = f.wslot[q];
   // CTA-pair kernels need d % 256 == 0 and an even grid; AMOE_FFN_1CTA=1 forces 1-CTA, =0 pairs
@@ -1346,6 +1467,7 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   const bool cold = f.rows_hint > 0 && f.rows_hint <= 128 && !gathered;
   const bool pair = !force1 && !cold && c.d % 256 == 0 && num_sms >= 2;
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
+  if (!pair && a.gather == 2) a.gather = 1;   // the cp.async gather is built into the pair kernel only
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
     a.n_tiles = c.ff / 128;
     a.k_blocks = c.d / BK;

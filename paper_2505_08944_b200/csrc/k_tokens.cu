@@ -190,24 +190,30 @@ __device__ __forceinline__ void make_legs(const DevCtx& c, int layer, int slot, 
 
 // ---------------------------------------------------------------------------- RMSNorm (c7)
 // x = store(h / sqrt(mean(h^2) + eps)) for one row held at `h` (storage T), warp-cooperative.
-template <typename T>
+// The row was just stored by these lanes; it is re-read RB 16-B chunks per lane at a time, all
+// loads of a batch before its stores (h and x may alias as far as the compiler knows, so a
+// load-store loop would pay one L2 round trip per chunk: d / 256 of them per token).
+template <typename T, int RB = 4>
 __device__ __forceinline__ void rmsnorm_row(const DevCtx& c, const T* h, T* x, float ss, int lane) {
   using V = Vec<T>;
+  constexpr int STEP = kWarp * V::N;
   const float r = 1.0f / sqrtf(ss / (float)c.d + c.eps);
-  for (int col0 = lane * V::N; col0 < c.d; col0 += kU * kWarp * V::N) {
-    float f[kU][V::N];
+  for (int col0 = lane * V::N; col0 < c.d; col0 += RB * STEP) {
+    uint4 raw[RB];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int col = col0 + u * kWarp * V::N;
-      if (col < c.d) V::load(h + col, f[u]);
+    for (int u = 0; u < RB; ++u) {
+      const int col = col0 + u * STEP;
+      if (col < c.d) raw[u] = *reinterpret_cast<const uint4*>(h + col);
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int col = col0 + u * kWarp * V::N;
+    for (int u = 0; u < RB; ++u) {
+      const int col = col0 + u * STEP;
       if (col < c.d) {
+        float f[V::N];
+        V::unpack(raw[u], f);
 #pragma unroll
-        for (int j = 0; j < V::N; ++j) f[u][j] = f[u][j] * r;
-        V::store(x + col, f[u]);
+        for (int j = 0; j < V::N; ++j) f[j] = f[j] * r;
+        V::store(x + col, f);
       }
     }
   }
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
         for (int j = 0; j < V::N; ++j) { const float r = V::round(acc[j]); ss += r * r; }
       }
       ss = warp_sum(ss);
-      rmsnorm_row<T>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);
+      rmsnorm_row<T, (KSM >= 8 ? 4 : 2)>(c, h, xbase + (uint64_t)slot * c.d, ss, lane);
       if (lane == 0) { tlayer[slot] = layer; tpass[slot] = pass; atomicAdd(&s_merged, 1ull); }
       if (retire) {
         if (lane == 0) {

@@ -115,14 +115,19 @@ def test_fused_forward_equals_separate_forward(pair):
     assert m0 == m1 == P.T and l0 == l1 == P.T * P.K
 
 
-@pytest.mark.parametrize("pair,d,S", [("0", 512, 0), ("1", 512, 0), ("1", 2048, 2)])
-def test_fused_gather_equals_materialised_gather(pair, d, S):
-    """amoe_rebatch_ffn_forward (gather inside the gate/up A load via TMA tile::gather4, legs read
-    from the rings, forward inside the down epilogue) == rebatch + expert_ffn + forward, bitwise:
-    same pool rows, same merged tokens, same counts; ragged queue tails included."""
-    P = Problem(L=2, E=8, K=2, S=S, d=d, ff=1408 if d == 2048 else 1024, T=1000, seed=15)
+@pytest.mark.parametrize("pair,d,S,T,how", [("0", 512, 0, 1000, "tma4"), ("1", 512, 0, 1000, "tma4"),
+                                             ("1", 2048, 2, 1000, "tma4"), ("1", 512, 0, 1000, "cp"),
+                                             ("1", 2048, 2, 1000, "cp"), ("1", 2048, 2, 3001, "cp"),
+                                             ("1", 4096, 0, 2500, "cp")])
+def test_fused_gather_equals_materialised_gather(pair, d, S, T, how):
+    """amoe_rebatch_ffn_forward (gather inside the gate/up A load — TMA tile::gather4, or the
+    producer warp's cp.async copies (AMOE_CP_GATHER=1) — legs read from the rings, forward inside the
+    down epilogue) == rebatch + expert_ffn + forward, bitwise: same pool rows, same merged
+    tokens, same counts; ragged queue tails and several M tiles per queue included."""
+    ff = {512: 1024, 2048: 1408, 4096: 2048}[d]
+    P = Problem(L=2, E=8, K=2, S=S, d=d, ff=ff, T=T, seed=15)
     os.environ["AMOE_FFN_1CTA"] = "1" if pair == "0" else "0"
-    os.environ["AMOE_FUSED_GATHER"] = "1"
+    os.environ["AMOE_FUSED_GATHER" if how == "tma4" else "AMOE_CP_GATHER"] = "1"
     try:
         res = []
         for fused in (False, True):
@@ -149,7 +154,8 @@ def test_fused_gather_equals_materialised_gather(pair, d, S):
             res.append((pool, to_np(st["h"]), int(st["stats"][0])))
     finally:
         os.environ.pop("AMOE_FFN_1CTA")
-        os.environ.pop("AMOE_FUSED_GATHER")
+        os.environ.pop("AMOE_FUSED_GATHER", None)
+        os.environ.pop("AMOE_CP_GATHER", None)
     (p0, h0, m0), (p1, h1, m1) = res
     assert m0 == m1 == P.T
     assert np.array_equal(p0, p1) and np.array_equal(h0, h1)
