@@ -30,11 +30,6 @@ __device__ __forceinline__ int chunk_tokens(int n) {
   return tpc < kTokWarps ? kTokWarps : (tpc > kTPC ? kTPC : tpc);
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-               :: "r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))), "l"(gsrc) : "memory");
-}
-
 struct PendingLeg {
   int32_t r;      // owner rank (-1 = inactive)
   int32_t q;      // queue index on the owner
@@ -411,9 +406,6 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
   __shared__ int s_gslot[GATE ? kTPC : 1], s_glayer[GATE ? kTPC : 1], s_gpass[GATE ? kTPC : 1];
   __shared__ int s_guni;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // per-warp merge stage: [2 buffers][h + KSM legs][32 lanes] x 16 B (dynamic smem)
-  extern __shared__ __align__(16) uint4 s_merge_stage[];
-  uint4* my_stage = s_merge_stage + warp * 2 * (KSM + 1) * kWarp;
   const int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
   const int n = info[0];
   const uint32_t start = (uint32_t)info[1];
@@ -464,41 +456,21 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
       T* h = hbase + (uint64_t)slot * c.d;
       const T* legrow = pool + (uint64_t)slot * c.KS * c.d;
       float ss = 0.f;
-      // The h chunk and the K+S leg chunks of column chunk i+1 are copied into this warp's smem
-      // stage (cp.async, each lane its own 16-B slots) while chunk i is merged: two chunks of
-      // loads in flight per lane instead of one, without holding them in registers (the
-      // combine is latency-bound at the power-capped clock)
-      constexpr int STEP = kWarp * V::N;
-      const int nit = (c.d + STEP - 1) / STEP;
-      auto issue = [&](int it) {
-        const int col = it * STEP + lane * V::N;
-        uint4* st = my_stage + (it & 1) * (KSM + 1) * kWarp + lane;
-        if (col < c.d) {
-          cp_async16(st, h + col);
+      for (int col = lane * V::N; col < c.d; col += kWarp * V::N) {
+        // all K+S legs of this 16-byte chunk are loaded before the (ordered) accumulation, so
+        // each lane keeps K+S+1 loads in flight (the leg count is a runtime value <= KSM)
+        uint4 raw[KSM];
+        const uint4 hraw = *reinterpret_cast<const uint4*>(h + col);
 #pragma unroll
-          for (int k = 0; k < KSM; ++k)
-            if (k < c.KS) cp_async16(st + (k + 1) * kWarp, legrow + (uint64_t)k * c.d + col);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-      issue(0);
-      for (int it = 0; it < nit; ++it) {
-        if (it + 1 < nit) {
-          issue(it + 1);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        const int col = it * STEP + lane * V::N;
-        if (col >= c.d) continue;
-        const uint4* st = my_stage + (it & 1) * (KSM + 1) * kWarp + lane;
+        for (int k = 0; k < KSM; ++k)
+          if (k < c.KS) raw[k] = *reinterpret_cast<const uint4*>(legrow + (uint64_t)k * c.d + col);
         float acc[V::N];
-        V::unpack(st[0], acc);
+        V::unpack(hraw, acc);
 #pragma unroll
         for (int k = 0; k < KSM; ++k) {
           if (k < c.KS) {
             float o[V::N];
-            V::unpack(st[(k + 1) * kWarp], o);
+            V::unpack(raw[k], o);
             const float wk = w[k];
 #pragma unroll
             for (int j = 0; j < V::N; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(wk, o[j]));
@@ -792,16 +764,14 @@ static void launch_combine_t(const DevCtx& c, int retire_pass, int num_sms, cuda
   // homed tokens ready); CTAs loop over 32-token chunks of the ready list. Occupancy is a
   // property of the kernel (same on every B200); the SM count is the context's (AMOE_NUM_SMS
   // partitions in the G-rank emulation)
-  constexpr size_t smem = (size_t)kTokWarps * 2 * (KSM + 1) * kWarp * 16;   // merge stages
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(combine_kernel<T, KSM, GATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, combine_kernel<T, KSM, GATE>, kTokThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, combine_kernel<T, KSM, GATE>, kTokThreads, 0);
     if (occ < 1) occ = 1;
   }
   int grid = (c.T + kTPC - 1) / kTPC;
   if (grid > num_sms * occ) grid = num_sms * occ;
-  launch_pdl(combine_kernel<T, KSM, GATE>, dim3(grid), dim3(kTokThreads), smem, s, c, retire_pass);
+  launch_pdl(combine_kernel<T, KSM, GATE>, dim3(grid), dim3(kTokThreads), 0, s, c, retire_pass);
 }
 
 template <typename T, bool GATE>
