@@ -198,7 +198,9 @@ def test_run_tiny_matches_oracle(dtype, policy, grouped):
     W, SH = P.oracle_weights()
     h0 = host_values(P.h0[0], dtype)
     ref, _ = drivers.sync_run(h0, P.logits, W, P.K, n_passes=passes, shared=SH, dtype=dtype)
-    assert floored_err(h_gpu, ref) <= TOL[dtype] * (1 if dtype == "bf16" else 10)
+    # free-running over 2 layers x 2 passes, fp32 included at the contract's 1e-5 (measured
+    # 1.2-1.5e-6 on B200: profiles/r02/fp32_freerun.jsonl)
+    assert floored_err(h_gpu, ref) <= TOL[dtype]
     qctr = ctx.state()["qctr"].cpu().numpy()
     assert np.all(qctr[..., 0] == qctr[..., 1]) and np.all(qctr[..., 1] == qctr[..., 2])
     assert np.all(qctr[..., 2].sum(axis=1) == P.T * P.K * passes)
