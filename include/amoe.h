@@ -310,9 +310,25 @@ amoe_status amoe_forward(amoe_ctx_t ctx, const amoe_group* grp, void* stream);
  * else route with the router table and enqueue. */
 amoe_status amoe_combine(amoe_ctx_t ctx, int retire_pass, void* stream);
 
-/* Run the asynchronous scheduler loop (host C++) until every token of every rank has retired
- * at pass `retire_pass`: poll depths, pick (Algorithm 1 / MTFS / FLFS), rebatch, expert_ffn,
- * forward, combine. Multi-GPU: keeps serving peers until all ranks report done. */
+/* Run the asynchronous scheduler loop (host C++; "whenever the GPU becomes idle",
+ * Algorithm 1) until every token of every rank has retired at pass `retire_pass`:
+ * read the queue counters, pick (params->policy: Algorithm 1 with lookahead W and δ, MTFS,
+ * FLFS, the lockstep SYNC baseline, or Algorithm 1 with the box-wide lookahead), execute, merge.
+ * A pick is one (layer, expert) queue, or with params->grouped every nonempty hosted queue of
+ * the picked layer. Execution: a cold pick (every queue <= 16 legs, <= 32 for Mixtral-sized
+ * experts or groups of >= 4; bf16, d % 256 == 0) runs amoe_execute_cold, otherwise
+ * amoe_rebatch_ffn_forward; then amoe_combine. Asynchronous policies pipeline the loop: the host
+ * decides pick k + 1 from an asynchronous counter snapshot while pick k runs (every drain takes
+ * exactly the host's count); AMOE_PIPELINE=0 synchronises after each pick.
+ * params->max_picks > 0 (single rank, not SYNC): return after that many picks or when nothing is
+ * runnable (open-loop stepping; the caller admits new tokens between calls).
+ * Returns AMOE_OK; AMOE_EINVAL for bad params, a missing router (neither table nor gate), a
+ * hosted queue without weights, SYNC with stepping, stepping at G > 1; AMOE_EPEER before
+ * amoe_import_peers at G > 1; AMOE_EDEVICE when a device fault is latched (amoe_error_info):
+ * any kernel fault, a lost leg at G = 1 (code 11, naming the stranded token), a peer's fault at
+ * G > 1 (code 9: the faulting rank stores an abort mark into every peer, so every rank returns),
+ * or AMOE_RUN_TIMEOUT seconds (default 600) without completion at G > 1 (code 10). Multi-GPU:
+ * keeps serving peers until all ranks report done. stats may be NULL. */
 amoe_status amoe_run(amoe_ctx_t ctx, const amoe_run_params* params, int retire_pass,
                      amoe_run_stats* stats, void* stream);
 

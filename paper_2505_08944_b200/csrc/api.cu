@@ -924,6 +924,13 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
     }
   cudaStream_t s = (cudaStream_t)stream;
   c->last_stream = s;
+  // the per-pick drain counts (c->exact_caps) point into this frame: cleared on every return,
+  // including the error returns between a pick's launches, so a later public amoe_rebatch call
+  // never reads a dead pick's caps
+  struct ExactCapsReset {
+    amoe_ctx* c;
+    ~ExactCapsReset() { c->exact_caps = nullptr; }
+  } exact_caps_reset{c};
   amoe_run_stats rs{};
   const uint32_t epoch = ++c->epoch;
   const int64_t expected = c->admitted;
