@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 export AMOE_DIE_PROBE=0
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck synccheck racecheck; do
-  for what in single loopback; do
+  for what in single loopback cold direct global; do
     timeout 900 $CS --tool $tool --print-limit 50 --error-exitcode 9 \
       python tools/sanitize_run.py $what > gpurun_out/sanitize_${tool}_${what}.log 2>&1
     echo "$tool $what rc=$?" | tee -a gpurun_out/sanitize_summary.txt
