@@ -110,6 +110,9 @@ struct FfnLaunch {
   const CUtensorMap* wmaps;      // device [L*H][3]
   int wslot[AMOE_MAX_GROUP];     // (l*H + lq) * 3
   int rows_hint;                 // amoe_group::max_rows_hint
+  int exact_max_n = -1;          // amoe_run's pipelined picks: the largest queue's exact drain count
+                                 // (-1: unknown); a launch whose largest queue spans >= 2 M tiles
+                                 // never splits K, so its split-K reduction is not launched
 };
 
 template <typename T>

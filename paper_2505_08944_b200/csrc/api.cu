@@ -626,6 +626,10 @@ static amoe_status expert_ffn(amoe_ctx* c, const amoe_group* g, int fuse, cudaSt
     f.wmaps = reinterpret_cast<const CUtensorMap*>(c->ws + c->lay.wmaps);
     for (int q = 0; q < g->nq; ++q) f.wslot[q] = wslot[q];
     f.rows_hint = gathered ? 0 : g->max_rows_hint;
+    if (c->exact_caps) {
+      f.exact_max_n = 0;
+      for (int q = 0; q < g->nq; ++q) f.exact_max_n = std::max(f.exact_max_n, (int)c->exact_caps[q]);
+    }
     {
       StageTimer tm(c, ST_GATEUP, s);
       c->launches += launch_ffn_tc(c->dc, f, mt, ma, mt32, ma32, g->act, g->out, g->meta, 0, gathered, c->num_sms, s, 1);

@@ -1466,6 +1466,9 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
   // 0.70-0.77 (profiles/r01_rebatch_sweep.md)
   const bool cold = f.rows_hint > 0 && f.rows_hint <= 128 && !gathered;
   const bool pair = !force1 && !cold && c.d % 256 == 0 && num_sms >= 2;
+  // choose_split never splits a launch whose largest queue spans two M tiles: with the exact
+  // drain counts known (amoe_run's pipelined picks) the no-op reduction launch is skipped
+  const bool reduce = f.exact_max_n < 0 || f.exact_max_n <= (pair ? 256 : 128);
   const int bn = pair ? 256 : ((c.d % 256 == 0) ? 256 : 128);
   if (!pair && a.gather == 2) a.gather = 1;   // the cp.async gather is built into the pair kernel only
   if (part == 1) {            // N tiles of 128 ff-columns (x2: gate and up)
@@ -1520,24 +1523,24 @@ int launch_ffn_tc(const DevCtx& c, const FfnLaunch& f, const CUtensorMap& tm_til
     const int slots = (num_sms & ~1) / 2;
     if (part == 1) {
       cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_GATEUP>, tm_tile, a, c);
-      if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_GATEUP, 256, true>, dim3(num_sms * 2), dim3(256), 0, s, a, c, slots);
+      if (a.allow_split && reduce) launch_pdl(splitk_reduce_kernel<MODE_GATEUP, 256, true>, dim3(num_sms * 2), dim3(256), 0, s, a, c, slots);
     } else {
       cudaLaunchKernelEx(&cfg, tc2::ffn_tc2_kernel<MODE_DOWN>, tm_act, a, c);
-      if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 256, true>, dim3(num_sms * 2), dim3(256), 0, s, a, c, slots);
+      if (a.allow_split && reduce) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 256, true>, dim3(num_sms * 2), dim3(256), 0, s, a, c, slots);
     }
-    return a.allow_split ? 2 : 1;
+    return a.allow_split && reduce ? 2 : 1;
   }
   if (part == 1) {
     launch_pdl(ffn_tc_kernel<MODE_GATEUP, 256>, dim3(num_sms), dim3(THREADS), SMEM_BYTES, s, tm_tile, tm_tile32, a, c);
-    if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_GATEUP, 256, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
+    if (a.allow_split && reduce) launch_pdl(splitk_reduce_kernel<MODE_GATEUP, 256, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
   } else if (bn == 256) {
     launch_pdl(ffn_tc_kernel<MODE_DOWN, 256>, dim3(num_sms), dim3(THREADS), SMEM_BYTES, s, tm_act, tm_act32, a, c);
-    if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 256, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
+    if (a.allow_split && reduce) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 256, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
   } else {
     launch_pdl(ffn_tc_kernel<MODE_DOWN, 128>, dim3(num_sms), dim3(THREADS), SMEM_BYTES, s, tm_act, tm_act32, a, c);
-    if (a.allow_split) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 128, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
+    if (a.allow_split && reduce) launch_pdl(splitk_reduce_kernel<MODE_DOWN, 128, false>, dim3(num_sms * 2), dim3(256), 0, s, a, c, num_sms);
   }
-  return a.allow_split ? 2 : 1;
+  return a.allow_split && reduce ? 2 : 1;
 }
 
 }  // namespace amoe
