@@ -395,7 +395,10 @@ def main():
     # ------------------------------------------------------------------ timed region
     clocks = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
-    ctx.profile_enable(True)
+    # per-stage CUDA events (the roofline's kernel times and the schedule's execution log) inside
+    # the timed region; AMOE_BENCH_STAGE_EVENTS=0 times the step without them (A/B of their cost)
+    stage_events = os.environ.get("AMOE_BENCH_STAGE_EVENTS", "1") != "0"
+    ctx.profile_enable(stage_events)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
