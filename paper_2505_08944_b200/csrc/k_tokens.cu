@@ -406,9 +406,25 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
   __shared__ int s_gslot[GATE ? kTPC : 1], s_glayer[GATE ? kTPC : 1], s_gpass[GATE ? kTPC : 1];
   __shared__ int s_guni;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
-  const int n = info[0];
-  const uint32_t start = (uint32_t)info[1];
+  int32_t* info = wsp<int32_t>(c, c.rank, c.lay.cinfo);
+  uint32_t* cctr = wsp<uint32_t>(c, c.rank, c.lay.cctr);
+  // G = 1: every entry of the combine ring was appended by this rank's earlier kernels (stream
+  // order), so each CTA reads the published prefix [head, commit) itself and the last CTA to
+  // finish advances the head (no cdrain launch); G > 1: cdrain_kernel's snapshot (peers may be
+  // appending concurrently)
+  int n;
+  uint32_t start;
+  if (c.G == 1) {
+    start = cctr[2];
+    n = (int)(ld_acquire(cctr + 1) - start);
+    if ((uint32_t)n > c.cring_cap) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) raise_fault(c, F_CRING_OVERFLOW, cctr[0], start, 0);
+      n = 0;
+    }
+  } else {
+    n = info[0];
+    start = (uint32_t)info[1];
+  }
   const amoe_leg* ring = wsp<amoe_leg>(c, c.rank, c.lay.cring);
   T* hbase = wsp<T>(c, c.rank, c.lay.h);
   T* xbase = wsp<T>(c, c.rank, c.lay.x);
@@ -567,6 +583,15 @@ __global__ void __launch_bounds__(kTokThreads, (KSM <= 4 && !GATE ? 4 : 2)) comb
     unsigned long long* st = wsp<unsigned long long>(c, c.rank, c.lay.stats);
     if (s_merged) atomicAdd(st + 0, s_merged);
     if (s_retired) atomicAdd(st + 1, s_retired);
+    if (c.G == 1) {
+      // every CTA has read the head: the last one out consumes the prefix (info[2]: exit count)
+      __threadfence();
+      if (atomicAdd(reinterpret_cast<uint32_t*>(info + 2), 1u) == gridDim.x - 1) {
+        cctr[2] = start + (uint32_t)n;
+        info[2] = 0;
+        __threadfence();
+      }
+    }
   }
 }
 
@@ -784,7 +809,7 @@ static void launch_combine_g(const DevCtx& c, int retire_pass, int num_sms, cuda
 }
 
 int launch_combine(const DevCtx& c, int retire_pass, int num_sms, cudaStream_t s) {
-  launch_pdl(cdrain_kernel, dim3(1), dim3(32), 0, s, c);
+  if (c.G > 1) launch_pdl(cdrain_kernel, dim3(1), dim3(32), 0, s, c);   // G = 1: inside the combine
   if (c.dtype == AMOE_BF16) {
     if (c.gate_on) launch_combine_g<__nv_bfloat16, true>(c, retire_pass, num_sms, s);
     else launch_combine_g<__nv_bfloat16, false>(c, retire_pass, num_sms, s);
@@ -792,7 +817,7 @@ int launch_combine(const DevCtx& c, int retire_pass, int num_sms, cudaStream_t s
     if (c.gate_on) launch_combine_g<float, true>(c, retire_pass, num_sms, s);
     else launch_combine_g<float, false>(c, retire_pass, num_sms, s);
   }
-  return 2;
+  return c.G > 1 ? 2 : 1;
 }
 
 int launch_announce(const DevCtx& c, uint32_t value, int base, cudaStream_t s) {

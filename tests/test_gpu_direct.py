@@ -58,15 +58,17 @@ def test_direct_top1_matches_oracle_and_pooled(dtype, monkeypatch):
     W, SH = P.oracle_weights()
     ref, _ = drivers.sync_run(host_values(P.h0[0], dtype), P.logits, W, P.K, n_passes=passes, shared=SH,
                               dtype=dtype)
-    tol = TOL[dtype] if dtype == "bf16" else 1e-4      # fp32: 4 free-running layers (reading c13)
-    assert floored_err(h, ref) <= tol
+    # free-running over 2 layers x 2 passes at the contract's tolerances
+    assert floored_err(h, ref) <= TOL[dtype]
     if dtype == "bf16":
         assert row_l2_err(h, ref) <= ROW_L2["bf16"]
     _, stats0, h0, _ = _run(P, False, passes)
     assert stats0["token_layers"] == stats["token_layers"]
     assert np.array_equal(h, h0)
-    # the direct path launches no combine: fewer kernels per pick
-    assert stats["kernel_launches"] < stats0["kernel_launches"]
+    # the direct path launches no combine (its merge kernel replaces it): no more kernels per pick
+    # than the pooled path, whose combine-ring snapshot runs inside the combine at G = 1
+    assert stats["kernel_launches"] <= stats0["kernel_launches"]
+    assert int(st["stats"][0]) == P.T * P.L * passes      # every merge counted on the home
 
 
 def test_direct_requires_top1():
