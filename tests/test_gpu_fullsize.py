@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from oracle import numerics as nx
-from parity_util import Problem, TOL, dev_tensor, floored_err, host_values, row_l2_err, to_np
+from parity_util import ROW_L2, Problem, TOL, dev_tensor, floored_err, host_values, row_l2_err, to_np
 
 pytestmark = pytest.mark.gpu
 
@@ -225,7 +225,7 @@ def test_layer_fullsize_every_m_tile(shape):
       of its drained legs (each CTA's half of every 256-row pair tile, ragged tails included),
       plus its last row, is recomputed by the float64 oracle from the GPU's own x and compared,
       all columns, with the row the fused epilogue stored into the home token pool (floored 2e-2;
-      row-L2 mean <= 1e-3 and max <= 4e-3, reading c13).
+      row-L2 mean <= 2e-3 (reading c13's diagnostic) and max <= 4e-3).
     - The merge of every token is bit-exact (teacher-forced on the GPU's pool and weights) and
       x_{l+1} is within one bf16 ulp of rmsnorm(h)."""
     from parity_util import replay_exec_log, ulp_err
@@ -268,7 +268,11 @@ def test_layer_fullsize_every_m_tile(shape):
         got = pool[sl, ks]
         assert floored_err(got, ref) <= TOL["bf16"], (e, floored_err(got, ref))
         rl2 = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
-        assert rl2.mean() <= 1e-3 and rl2.max() <= 4e-3, (e, rl2.mean(), rl2.max())   # reading c13
+        # reading c13's diagnostic (mean row-L2 <= 2e-3): bf16 output rounding alone puts a row's
+        # relative L2 error near 1e-3, so a mean over a few randomly sampled rows at 1e-3 (this
+        # test's former gate, tighter than c13) fails by chance (1.07e-3 on expert 13 of a DeepSeek
+        # layer, profiles/r02/final/pytest_gpu.log)
+        assert rl2.mean() <= ROW_L2["bf16"] and rl2.max() <= 4e-3, (e, rl2.mean(), rl2.max())
         checked += len(rows)
     assert checked >= sum(-(-len(x[3]) // 128) for x in log)
     w_gpu = st["tok_w"].cpu().numpy()
