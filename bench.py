@@ -36,8 +36,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=["mixtral", "deepseek", "tiny"])
-    ap.add_argument("--policy", default="defrag", choices=["defrag", "mtfs", "flfs", "sync", "defrag_global"],
-                    help="sync = synchronous-EP baseline: lockstep layers, box-wide barrier per layer")
+    ap.add_argument("--policy", default="defrag_global", choices=["defrag", "mtfs", "flfs", "sync", "defrag_global"],
+                    help="defrag_global = Algorithm 1 with the box-wide lookahead (identical to defrag on one "
+                         "GPU; ahead of it at G > 1 in the G-rank emulation); sync = synchronous-EP baseline: "
+                         "lockstep layers, box-wide barrier per layer")
     ap.add_argument("--ungrouped", action="store_true", help="one (layer, expert) queue per launch")
     ap.add_argument("--T", type=int, default=0, help="override tokens in flight per GPU")
     ap.add_argument("--L", type=int, default=0, help="override layers (parity/debug only)")

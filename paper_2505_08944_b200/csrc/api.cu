@@ -955,20 +955,19 @@ amoe_status amoe_run(amoe_ctx_t c, const amoe_run_params* p, int retire_pass, am
   int idle_streak = 0;
   // AMOE_SYNC: the layer this rank may run, and whether it has arrived at that layer's barrier
   const bool sync = p->policy == AMOE_SYNC;
-  // G > 1, asynchronous policies, ranks hosting >= 2 routed experts (a grouped pick has
-  // something to consolidate), two changes to what the scheduler sees when the GPU goes idle:
-  // - merge first: pending merges (tokens whose last legs came back from other ranks) run
-  //   before the next pick, so their next-layer legs join it (AMOE_COMBINE_FIRST=1/0 forces);
-  // - grow wait: a pick is deferred while its layer's hosted depth still grows between polls
-  //   (legs streaming in from a peer's merge), at most AMOE_GROW_WAIT us (default 200; 0 off).
-  // G-rank emulation (profiles/r01_g_emulate.md): +3-23 % with 4-32 experts per rank, neutral
-  // with 2; with ONE expert per rank (Mixtral at G = 8) both slow the hot expert's rank, which
-  // is everyone's critical path (-12 %), so they stay off there. Deferrals count as idle.
-  const bool multi_expert = c->Hr >= 2;
+  // G > 1, asynchronous policies: two opt-in changes to what the scheduler sees when the GPU
+  // goes idle (both turn the pipelined loop off):
+  // - merge first (AMOE_COMBINE_FIRST=1): pending merges (tokens whose last legs came back from
+  //   other ranks) run before the next pick, so their next-layer legs join it;
+  // - grow wait (AMOE_GROW_WAIT=<us>): a pick is deferred while its layer's hosted depth still
+  //   grows between polls (legs streaming in from a peer's merge), at most that long.
+  // Round 1 measured them +3-23 % on the G-rank emulation for ranks hosting >= 2 experts and made
+  // them the default there; with round 2's pipelined loop the pipelined Algorithm 1 is ahead
+  // (Mixtral G = 2 1.30 vs 1.21 M, G = 4 1.06 vs 1.03 M; box-wide lookahead 1.31 / 1.09 M;
+  // profiles/r02/g_emulate_final.log), so both are off by default. Deferrals count as idle.
   const char* cf_env = getenv("AMOE_COMBINE_FIRST");
-  const bool combine_first = c->cfg.G > 1 && !sync && p->max_picks == 0 &&
-                             (cf_env ? cf_env[0] == '1' : multi_expert);
-  int64_t grow_ns = multi_expert ? 200000 : 0;
+  const bool combine_first = c->cfg.G > 1 && !sync && p->max_picks == 0 && cf_env && cf_env[0] == '1';
+  int64_t grow_ns = 0;
   if (const char* ge = getenv("AMOE_GROW_WAIT")) grow_ns = (int64_t)(atof(ge) * 1e3);
   if (c->cfg.G == 1 || sync || p->max_picks > 0) grow_ns = 0;
   std::vector<uint64_t> prev_depth(grow_ns > 0 ? c->cfg.L : 0, 0);

@@ -408,7 +408,8 @@ def test_box_depths_sum_every_rank(monkeypatch):
 
 @pytest.mark.parametrize("G,d,policy,sms", [(2, 128, "defrag", 0), (4, 256, "defrag", 0), (2, 128, "sync", 0),
                                              (4, 256, "sync", 0), (2, 256, "defrag", 74), (4, 256, "flfs", 36),
-                                             (2, 128, "defrag_global", 0), (4, 256, "defrag_global", 36)])
+                                             (2, 128, "defrag_global", 0), (4, 256, "defrag_global", 36),
+                                             (2, 128, "defrag_heur", 0), (4, 256, "defrag_heur", 0)])
 def test_loopback_amoe_run_concurrent_ranks(G, d, policy, sms, monkeypatch):
     """The native multi-rank loop: G contexts on one GPU, each running amoe_run in its own host
     thread on its own CUDA stream, concurrently. Legs cross ranks through peer rings (remote
@@ -420,6 +421,11 @@ def test_loopback_amoe_run_concurrent_ranks(G, d, policy, sms, monkeypatch):
     # fp32 accumulation order with the pick's shape (DESIGN.md §5.3/§5.4), so it is compared
     # within tolerance elsewhere (tests/test_gpu_cold.py); here every pick takes the unsplit path
     monkeypatch.setenv("AMOE_COLD", "0")
+    if policy == "defrag_heur":
+        # the opt-in G > 1 loop changes (merge first, grow wait: the synchronous loop)
+        monkeypatch.setenv("AMOE_COMBINE_FIRST", "1")
+        monkeypatch.setenv("AMOE_GROW_WAIT", "200")
+        policy = "defrag"
     import threading
     T = 128
     P = Problem(L=2, E=8, K=2, S=0, d=d, ff=256, T=T, G=G, seed=14)
