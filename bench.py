@@ -40,6 +40,8 @@ def parse():
                     help="defrag_global = Algorithm 1 with the box-wide lookahead (identical to defrag on one "
                          "GPU; ahead of it at G > 1 in the G-rank emulation); sync = synchronous-EP baseline: "
                          "lockstep layers, box-wide barrier per layer")
+    ap.add_argument("--W", type=int, default=4, help="Algorithm 1 lookahead depth (reading c11)")
+    ap.add_argument("--delta", type=float, default=0.5, help="Algorithm 1 lookahead decay (reading c11)")
     ap.add_argument("--ungrouped", action="store_true", help="one (layer, expert) queue per launch")
     ap.add_argument("--T", type=int, default=0, help="override tokens in flight per GPU")
     ap.add_argument("--L", type=int, default=0, help="override layers (parity/debug only)")
@@ -382,7 +384,7 @@ def main():
             ctx.enqueue(0, slots)
         else:
             ctx.enqueue(0, slots, logits=table[p % n_tab, 0])
-        return ctx.run(retire_pass=p + 1, policy=policy, grouped=grouped)
+        return ctx.run(retire_pass=p + 1, policy=policy, W=args.W, delta=args.delta, grouped=grouped)
 
     barrier = D.barrier
     # every rank must have created (zeroed) its workspace before any rank pushes legs into it
@@ -518,7 +520,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded Zipf s=1.2 routing, random-init bf16 weights)",
-        "config": config_dict(spec, L, T, G, policy, grouped, args.skew, args.router, args.direct, args.shift_every),
+        "config": dict(config_dict(spec, L, T, G, policy, grouped, args.skew, args.router, args.direct, args.shift_every),
+                       lookahead={"W": args.W, "delta": args.delta}),
         "gpu_launches": int(launches),
         "die_map_sms": list(amoe.die_info()),
         "clocks": clk,
@@ -549,13 +552,15 @@ def main():
         hout = torch.empty_like(h0_host).pin_memory()
         rt_host = [torch.from_numpy(t).pin_memory() for t in tables_host]
         for w in range(1):
-            ctx.pass_host(h0_host, hout, rt_host[w % n_tab], pass_idx=w, policy=policy, grouped=grouped)
+            ctx.pass_host(h0_host, hout, rt_host[w % n_tab], pass_idx=w, policy=policy, W=args.W, delta=args.delta,
+                          grouped=grouped)
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for k in range(args.steps):
-            ctx.pass_host(h0_host, hout, rt_host[k % n_tab], pass_idx=k, policy=policy, grouped=grouped)
+            ctx.pass_host(h0_host, hout, rt_host[k % n_tab], pass_idx=k, policy=policy, W=args.W, delta=args.delta,
+                          grouped=grouped)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
