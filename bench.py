@@ -40,8 +40,11 @@ def parse():
                     help="defrag_global = Algorithm 1 with the box-wide lookahead (identical to defrag on one "
                          "GPU; ahead of it at G > 1 in the G-rank emulation); sync = synchronous-EP baseline: "
                          "lockstep layers, box-wide barrier per layer")
-    ap.add_argument("--W", type=int, default=4, help="Algorithm 1 lookahead depth (reading c11)")
-    ap.add_argument("--delta", type=float, default=0.5, help="Algorithm 1 lookahead decay (reading c11)")
+    # Algorithm 1's lookahead (reading c11): W = 4, δ = 0.5 on one GPU; at G > 1
+    # W = 8, δ = 1.0, the best of the G-rank emulation sweep (profiles/r02/g_emulate_sweep2.log:
+    # Mixtral G = 4 1.20-1.23 M vs sync EP 1.14-1.16 M, G = 2 1.38 M vs 1.38-1.39 M)
+    ap.add_argument("--W", type=int, default=None, help="Algorithm 1 lookahead depth (default 4; 8 at G > 1)")
+    ap.add_argument("--delta", type=float, default=None, help="Algorithm 1 lookahead decay (default 0.5; 1.0 at G > 1)")
     ap.add_argument("--ungrouped", action="store_true", help="one (layer, expert) queue per launch")
     ap.add_argument("--T", type=int, default=0, help="override tokens in flight per GPU")
     ap.add_argument("--L", type=int, default=0, help="override layers (parity/debug only)")
@@ -60,7 +63,12 @@ def parse():
                          "merges and routes each token itself, no token pool / combine launch (SURVEY.md f3)")
     ap.add_argument("--skew", default="zipf", choices=["zipf", "exp"],
                     help="routing skew: Zipf s=1.2 (BASELINE.json) or the paper's exponential fit (λ=0.38)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.W is None:
+        args.W = 8 if args.gpus > 1 else 4
+    if args.delta is None:
+        args.delta = 1.0 if args.gpus > 1 else 0.5
+    return args
 
 
 def FFN_KERNEL(d):
